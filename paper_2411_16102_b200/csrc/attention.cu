@@ -1,0 +1,133 @@
+// attention.cu — blend_plan_upload and blend_attention: validates arguments and
+// enqueues the dense pass (tcgen05), the streaming pass and the LSE merge on the
+// caller's stream.  Never allocates, never synchronises.
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "blend.h"
+#include "common.cuh"
+
+extern "C" int blend_internal_fail(int status, const char* msg);
+extern "C" int blend_internal_plan_image(const blend_tree* t, const void** data, size_t* bytes, const int64_t** off,
+                                         const int64_t** count);
+extern "C" int blend_internal_tree_dims(const blend_tree* t, int32_t* dims);
+extern "C" int64_t blend_internal_partial_rows(const blend_tree* t);
+
+namespace blend {
+cudaError_t launch_generic(const AttnParams& p, cudaStream_t st);
+cudaError_t launch_merge(const AttnParams& p, cudaStream_t st);
+cudaError_t launch_stream(const AttnParams& p, int64_t n_cache_pages, cudaStream_t st);
+cudaError_t launch_dense(const AttnParams& p, int64_t n_cache_pages, cudaStream_t st);
+}  // namespace blend
+
+namespace {
+int cuda_fail(cudaError_t e) { return blend_internal_fail(BLEND_ECUDA, cudaGetErrorString(e)); }
+
+int check_arch() {
+  int dev = 0, major = 0, minor = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return cuda_fail(cudaGetLastError());
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  if (major != 10 || minor != 0) return blend_internal_fail(BLEND_EUNSUPPORTED, "libblend is built for sm_100a (B200)");
+  return BLEND_OK;
+}
+}  // namespace
+
+extern "C" int blend_plan_upload(const blend_tree* tree, void* dev_buf, size_t bytes, void* stream, blend_plan* plan) {
+  if (!tree || !dev_buf || !plan) return blend_internal_fail(BLEND_EINVAL, "plan_upload: NULL argument");
+  const void* data;
+  size_t need;
+  const int64_t *off, *count;
+  int st = blend_internal_plan_image(tree, &data, &need, &off, &count);
+  if (st) return st;
+  if (bytes < need) return blend_internal_fail(BLEND_ENOSPC, "plan_upload: buffer too small");
+  cudaError_t e = cudaMemcpyAsync(dev_buf, data, need, cudaMemcpyHostToDevice, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e);
+  plan->dev = dev_buf;
+  plan->bytes = need;
+  for (int i = 0; i < 16; ++i) {
+    plan->off[i] = off[i];
+    plan->count[i] = count[i];
+  }
+  plan->count[blend::SEC_COUNT] = blend_internal_partial_rows(tree);
+  int32_t dims[5];
+  blend_internal_tree_dims(tree, dims);
+  plan->num_q_heads = dims[0];
+  plan->num_kv_heads = dims[1];
+  plan->head_dim = dims[2];
+  plan->kv_dtype = dims[3];
+  plan->page_size = dims[4];
+  plan->reserved = 0;
+  return BLEND_OK;
+}
+
+extern "C" int blend_attention(const blend_attn_args* a, void* stream) {
+  using namespace blend;
+  if (!a || !a->plan || !a->q || !a->k_cache || !a->v_cache || !a->out || !a->lse)
+    return blend_internal_fail(BLEND_EINVAL, "attention: NULL argument");
+  const blend_plan& pl = *a->plan;
+  if (!pl.dev) return blend_internal_fail(BLEND_EINVAL, "attention: plan not uploaded");
+  if (a->path < 0 || a->path > 2) return blend_internal_fail(BLEND_EINVAL, "attention: bad path");
+  static int arch_ok = -1;
+  if (arch_ok < 0) arch_ok = check_arch() == BLEND_OK ? 1 : 0;
+  if (!arch_ok) return blend_internal_fail(BLEND_EUNSUPPORTED, "libblend is built for sm_100a (B200)");
+  const int64_t prow = pl.count[SEC_COUNT];
+  const int hq = pl.num_q_heads, D = pl.head_dim;
+  size_t o_bytes = ((size_t)prow * hq * D * 4 + 255) & ~size_t(255);
+  size_t need = o_bytes + (((size_t)prow * hq * 4 + 255) & ~size_t(255));
+  if (prow > 0 && (!a->workspace || a->workspace_bytes < need))
+    return blend_internal_fail(BLEND_ENOSPC, "attention: workspace too small");
+  if (a->n_cache_pages <= 0) return blend_internal_fail(BLEND_EINVAL, "attention: n_cache_pages");
+
+  const char* base = (const char*)pl.dev;
+  AttnParams p{};
+  p.q = a->q;
+  p.k_cache = a->k_cache;
+  p.v_cache = a->v_cache;
+  p.out = a->out;
+  p.lse = a->lse;
+  p.ws_o = (float*)a->workspace;
+  p.ws_lse = (float*)((char*)a->workspace + o_bytes);
+  p.tok_pos = (const int32_t*)(base + pl.off[SEC_TOK_POS]);
+  p.item_tokens = (const int32_t*)(base + pl.off[SEC_ITEM_TOKENS]);
+  p.entries = (const KvEntry*)(base + pl.off[SEC_ENTRIES]);
+  p.partmap = (const int32_t*)(base + pl.off[SEC_PARTMAP]);
+  p.merge_tok = (const int32_t*)(base + pl.off[SEC_MERGE_TOK]);
+  p.merge_off = (const int32_t*)(base + pl.off[SEC_MERGE_OFF]);
+  p.merge_rows = (const int32_t*)(base + pl.off[SEC_MERGE_ROWS]);
+  p.n_merge = (int32_t)pl.count[SEC_MERGE_TOK];
+  p.hq = hq;
+  p.hkv = pl.num_kv_heads;
+  p.g = hq / pl.num_kv_heads;
+  p.d = D;
+  p.ps = pl.page_size;
+  p.kv_f32 = pl.kv_dtype == BLEND_F32;
+  p.scale_log2 = kLog2e / sqrtf((float)D);
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool generic = a->path == BLEND_PATH_GENERIC || p.kv_f32;
+  cudaError_t e;
+
+  if (a->events[0]) cudaEventRecord((cudaEvent_t)a->events[0], st);
+  AttnParams pd = p;
+  pd.units = (const Unit*)(base + pl.off[SEC_DENSE_UNITS]);
+  pd.n_units = (int32_t)pl.count[SEC_DENSE_UNITS];
+  if (generic || a->path == BLEND_PATH_NO_TCGEN05) e = launch_generic(pd, st);
+  else e = launch_dense(pd, a->n_cache_pages, st);
+  if (e != cudaSuccess) return cuda_fail(e);
+
+  if (a->events[1]) cudaEventRecord((cudaEvent_t)a->events[1], st);
+  AttnParams ps_ = p;
+  ps_.units = (const Unit*)(base + pl.off[SEC_STREAM_UNITS]);
+  ps_.n_units = (int32_t)pl.count[SEC_STREAM_UNITS];
+  if (generic) e = launch_generic(ps_, st);
+  else e = launch_stream(ps_, a->n_cache_pages, st);
+  if (e != cudaSuccess) return cuda_fail(e);
+
+  if (a->events[2]) cudaEventRecord((cudaEvent_t)a->events[2], st);
+  e = launch_merge(p, st);
+  if (e != cudaSuccess) return cuda_fail(e);
+  if (a->events[3]) cudaEventRecord((cudaEvent_t)a->events[3], st);
+  e = cudaPeekAtLastError();
+  if (e != cudaSuccess) return cuda_fail(e);
+  return BLEND_OK;
+}

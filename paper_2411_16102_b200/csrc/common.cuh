@@ -1,0 +1,77 @@
+// common.cuh — device helpers shared by libblend's kernels.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "internal.h"
+
+namespace blend {
+
+constexpr float kLn2 = 0.6931471805599453f;
+constexpr float kLog2e = 1.4426950408889634f;
+
+// Pointers + dims every attention kernel needs (passed by value).
+struct AttnParams {
+  const void* q;
+  const void* k_cache;
+  const void* v_cache;
+  void* out;
+  float* lse;
+  float* ws_o;      // [partial rows][Hq][D] fp32
+  float* ws_lse;    // [partial rows][Hq]    fp32, log2 domain
+  const int32_t* tok_pos;
+  const int32_t* item_tokens;
+  const KvEntry* entries;
+  const Unit* units;
+  const int32_t* partmap;
+  const int32_t* merge_tok;
+  const int32_t* merge_off;
+  const int32_t* merge_rows;
+  int32_t n_units;
+  int32_t n_merge;
+  int32_t hq, hkv, g, d, ps;
+  int32_t kv_f32;   // 1: fp32 q/k/v/out, 0: bf16
+  float scale_log2; // log2(e) / sqrt(D)
+};
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ float grid_val(uint64_t z) { return (float)((int)(z >> 56) - 128) * (1.0f / 128.0f); }
+
+__device__ __forceinline__ float ld_elem(const void* base, int64_t idx, int f32) {
+  return f32 ? __ldg(reinterpret_cast<const float*>(base) + idx)
+             : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(base)[idx]);
+}
+
+__device__ __forceinline__ void st_elem(void* base, int64_t idx, float v, int f32) {
+  if (f32) reinterpret_cast<float*>(base)[idx] = v;
+  else reinterpret_cast<__nv_bfloat16*>(base)[idx] = __float2bfloat16_rn(v);
+}
+
+// Row metadata of unit row r: global token, q head, token_local
+struct RowInfo {
+  int32_t token, head, tl;
+};
+__device__ __forceinline__ RowInfo row_info(const AttnParams& p, const Unit& u, int r) {
+  int ir = u.row_begin + r;
+  int tl = ir / p.g;
+  RowInfo ri;
+  ri.tl = tl;
+  ri.token = p.item_tokens[u.tok_base + tl];
+  ri.head = u.kvh * p.g + (ir - tl * p.g);
+  return ri;
+}
+
+// Write one finished row: O already normalised, lse2 in log2 units (-inf if empty).
+// DIRECT -> out/lse (natural log); partial row -> workspace; SKIP -> nothing.
+__device__ __forceinline__ int32_t row_target(const AttnParams& p, const Unit& u, int tl) {
+  return p.partmap[u.pm_base + tl];
+}
+
+}  // namespace blend

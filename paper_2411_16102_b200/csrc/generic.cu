@@ -1,0 +1,179 @@
+// generic.cu — the generic item executor (fp32 FMA, any row count <= 128, per-row
+// causal mask) and the LSE-merge epilogue.
+//
+// The generic executor runs ANY work unit of the plan: it is the fp32 debug path
+// (tcgen05 has no fp32 kind) and the reference executor the optimised kernels
+// are checked against (BLEND_PATH_GENERIC).  Per unit it computes, for each row
+// (query token, q head) and the unit's keys K_e (a contiguous range of the
+// item's page entries):
+//     s = q . k / sqrt(D)  (visible iff key_pos <= row_pos),  online softmax,
+//     o = sum softmax(s) v, lse2 = log2-sum-exp2 of s*log2(e)
+// exactly the per-partial quantity of the cascade (PAPER §7.2).
+//
+// The merge epilogue combines a token's partials in ascending key-range order
+// (reading #17): L = max lse_i + log sum exp(lse_i - max), O = sum exp(lse_i - L) o_i.
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "blend.h"
+#include "common.cuh"
+
+namespace blend {
+
+constexpr int GEN_ROWS = 128;
+constexpr int GEN_KT = 32;
+
+__device__ __forceinline__ void write_row(const AttnParams& p, const RowInfo& ri, int32_t tgt, const float* o,
+                                          float inv_l, float lse2, int lane_stride, int lane) {
+  if (tgt == PM_SKIP) return;
+  if (tgt == PM_DIRECT) {
+    int64_t base = ((int64_t)ri.token * p.hq + ri.head) * p.d;
+    for (int e = lane; e < p.d; e += lane_stride) st_elem(p.out, base + e, o[e] * inv_l, p.kv_f32);
+    if (lane == 0) p.lse[(int64_t)ri.token * p.hq + ri.head] = lse2 * kLn2;
+  } else {
+    int64_t base = ((int64_t)tgt * p.hq + ri.head) * p.d;
+    for (int e = lane; e < p.d; e += lane_stride) p.ws_o[base + e] = o[e] * inv_l;
+    if (lane == 0) p.ws_lse[(int64_t)tgt * p.hq + ri.head] = lse2;
+  }
+}
+
+// One CTA (128 threads) per unit.  Dynamic smem (fp32):
+//   qs[128][D] | os[128][D] | ks[KT][D+1] | vs[KT][D] | ss[128][KT+1] | m,l,alpha[128] | pos[128]
+__global__ void __launch_bounds__(128) generic_unit_kernel(AttnParams p) {
+  extern __shared__ float sm[];
+  const int D = p.d;
+  float* qs = sm;
+  float* os = qs + GEN_ROWS * D;
+  float* ks = os + GEN_ROWS * D;
+  float* vs = ks + GEN_KT * (D + 1);
+  float* ss = vs + GEN_KT * D;
+  float* mrow = ss + GEN_ROWS * (GEN_KT + 1);
+  float* lrow = mrow + GEN_ROWS;
+  float* arow = lrow + GEN_ROWS;
+  int* prow = reinterpret_cast<int*>(arow + GEN_ROWS);
+
+  const Unit u = p.units[blockIdx.x];
+  const int nr = u.n_rows;
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < nr * D; idx += blockDim.x) {
+    int r = idx / D, e = idx % D;
+    RowInfo ri = row_info(p, u, r);
+    qs[idx] = ld_elem(p.q, ((int64_t)ri.token * p.hq + ri.head) * D + e, p.kv_f32) * p.scale_log2;
+    os[idx] = 0.f;
+  }
+  for (int r = tid; r < nr; r += blockDim.x) {
+    RowInfo ri = row_info(p, u, r);
+    prow[r] = p.tok_pos[ri.token];
+    mrow[r] = -INFINITY;
+    lrow[r] = 0.f;
+  }
+  __syncthreads();
+
+  for (int ei = u.entry_begin; ei < u.entry_end; ++ei) {
+    const KvEntry en = p.entries[ei];
+    const int64_t kvbase = (((int64_t)en.page * p.hkv + u.kvh) * p.ps + en.row_off) * D;
+    for (int k0 = 0; k0 < en.count; k0 += GEN_KT) {
+      const int kt = min(GEN_KT, en.count - k0);
+      for (int idx = tid; idx < kt * D; idx += blockDim.x) {
+        int i = idx / D, e = idx % D;
+        ks[i * (D + 1) + e] = ld_elem(p.k_cache, kvbase + (int64_t)(k0 + i) * D + e, p.kv_f32);
+        vs[i * D + e] = ld_elem(p.v_cache, kvbase + (int64_t)(k0 + i) * D + e, p.kv_f32);
+      }
+      __syncthreads();
+      for (int idx = tid; idx < nr * kt; idx += blockDim.x) {
+        int r = idx / kt, i = idx % kt;
+        float s = 0.f;
+        const float* qr = qs + r * D;
+        const float* kr = ks + i * (D + 1);
+        for (int e = 0; e < D; ++e) s = fmaf(qr[e], kr[e], s);
+        ss[r * (GEN_KT + 1) + i] = (en.pos0 + k0 + i <= prow[r]) ? s : -INFINITY;
+      }
+      __syncthreads();
+      for (int r = tid; r < nr; r += blockDim.x) {
+        float* sr = ss + r * (GEN_KT + 1);
+        float mx = mrow[r];
+        for (int i = 0; i < kt; ++i) mx = fmaxf(mx, sr[i]);
+        float alpha = 1.f, sum = 0.f;
+        if (mx == -INFINITY) {
+          for (int i = 0; i < kt; ++i) sr[i] = 0.f;
+        } else {
+          alpha = exp2f(mrow[r] - mx);   // m = -inf -> 0
+          for (int i = 0; i < kt; ++i) {
+            float pv = exp2f(sr[i] - mx);
+            sr[i] = pv;
+            sum += pv;
+          }
+        }
+        lrow[r] = lrow[r] * alpha + sum;
+        mrow[r] = mx;
+        arow[r] = alpha;
+      }
+      __syncthreads();
+      for (int idx = tid; idx < nr * D; idx += blockDim.x) {
+        int r = idx / D, e = idx % D;
+        const float* sr = ss + r * (GEN_KT + 1);
+        float o = os[idx] * arow[r];
+        for (int i = 0; i < kt; ++i) o = fmaf(sr[i], vs[i * D + e], o);
+        os[idx] = o;
+      }
+      __syncthreads();
+    }
+  }
+  // finalise: one warp per row
+  const int warp = tid >> 5, lane = tid & 31;
+  for (int r = warp; r < nr; r += blockDim.x / 32) {
+    RowInfo ri = row_info(p, u, r);
+    int32_t tgt = row_target(p, u, ri.tl);
+    float l = lrow[r];
+    float lse2 = l > 0.f ? mrow[r] + log2f(l) : -INFINITY;
+    float inv = l > 0.f ? 1.f / l : 0.f;
+    write_row(p, ri, tgt, os + r * D, inv, lse2, 32, lane);
+  }
+}
+
+// One CTA per merged token; threads stride over (head, element).
+__global__ void __launch_bounds__(256) merge_kernel(AttnParams p) {
+  const int m = blockIdx.x;
+  const int token = p.merge_tok[m];
+  const int s0 = p.merge_off[m], s1 = p.merge_off[m + 1];
+  const int D = p.d;
+  for (int idx = threadIdx.x; idx < p.hq * D; idx += blockDim.x) {
+    const int h = idx / D, e = idx % D;
+    float mx = -INFINITY;
+    for (int s = s0; s < s1; ++s) mx = fmaxf(mx, p.ws_lse[(int64_t)p.merge_rows[s] * p.hq + h]);
+    float o = 0.f, tot = 0.f;
+    if (mx != -INFINITY) {
+      for (int s = s0; s < s1; ++s) {
+        const int64_t row = p.merge_rows[s];
+        float w = exp2f(p.ws_lse[row * p.hq + h] - mx);
+        tot += w;
+        o = fmaf(w, p.ws_o[(row * p.hq + h) * D + e], o);
+      }
+      o /= tot;
+    }
+    st_elem(p.out, ((int64_t)token * p.hq + h) * D + e, o, p.kv_f32);
+    if (e == 0) p.lse[(int64_t)token * p.hq + h] = mx != -INFINITY ? (mx + log2f(tot)) * kLn2 : -INFINITY;
+  }
+}
+
+size_t generic_smem_bytes(int D) {
+  return sizeof(float) * ((size_t)GEN_ROWS * D * 2 + GEN_KT * (D + 1) + GEN_KT * D + GEN_ROWS * (GEN_KT + 1) +
+                          4 * GEN_ROWS);
+}
+
+cudaError_t launch_generic(const AttnParams& p, cudaStream_t st) {
+  if (p.n_units <= 0) return cudaSuccess;
+  size_t smem = generic_smem_bytes(p.d);
+  cudaError_t e = cudaFuncSetAttribute(generic_unit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  generic_unit_kernel<<<p.n_units, 128, smem, st>>>(p);
+  return cudaPeekAtLastError();
+}
+
+cudaError_t launch_merge(const AttnParams& p, cudaStream_t st) {
+  if (p.n_merge <= 0) return cudaSuccess;
+  merge_kernel<<<p.n_merge, 256, 0, st>>>(p);
+  return cudaPeekAtLastError();
+}
+
+}  // namespace blend

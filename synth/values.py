@@ -91,3 +91,14 @@ def q_values(global_req: int, t: np.ndarray, seed: int, num_q_heads: int, head_d
             * np.uint64(1 << 12) + e
         z = mix(seed_q ^ mix(ctr))
     return scale_q * grid(z)
+
+
+def segment_hash(tokens: np.ndarray, start: int, h_prev: int, seed: int) -> np.ndarray:
+    """H_j for j = start .. start+len(tokens)-1 of a path whose prefix hash at
+    position start-1 is h_prev (0 for start = 0): the per-node form of prefix_hash."""
+    tok = np.asarray(tokens, dtype=np.int64).astype(np.uint64)
+    pos = np.arange(start, start + tok.shape[0], dtype=np.uint64)
+    leaf = mix((tok << np.uint64(32)) ^ pos ^ np.uint64(seed & 0xFFFFFFFFFFFFFFFF))
+    if leaf.size == 0:
+        return leaf
+    return np.bitwise_xor.accumulate(leaf) ^ np.uint64(h_prev)

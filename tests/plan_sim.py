@@ -1,0 +1,97 @@
+"""CPU interpreter of libblend's device plan (test infrastructure).
+
+Reads the plan image the C++ planner produced (internal symbol
+blend_internal_plan_image), executes every work unit in fp64 numpy exactly as
+the kernels are specified to (keys of the unit's page entries, per-row causal
+mask, partial (o, lse) or direct write per the partmap), merges the partials
+in the plan's order, and returns (out, lse) — so the host planner is checked
+against the oracle without a GPU."""
+import ctypes as C
+
+import numpy as np
+
+import paper_2411_16102_b200 as B
+from harness.run import page_slot_hashes, query_rows
+from oracle import attention as A
+from synth import values as V
+
+SEC = ["tok_pos", "item_tok_off", "item_tokens", "entries", "dunits", "sunits", "partmap",
+       "merge_tok", "merge_off", "merge_rows"]
+
+
+def plan_image(tree):
+    L = B.lib()
+    f = L.blend_internal_plan_image
+    f.restype = C.c_int
+    f.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t),
+                  C.POINTER(C.POINTER(C.c_int64)), C.POINTER(C.POINTER(C.c_int64))]
+    data, nbytes = C.c_void_p(), C.c_size_t()
+    off, cnt = C.POINTER(C.c_int64)(), C.POINTER(C.c_int64)()
+    assert f(tree.handle, C.byref(data), C.byref(nbytes), C.byref(off), C.byref(cnt)) == 0
+    blob = np.ctypeslib.as_array(C.cast(data, C.POINTER(C.c_uint8)), (nbytes.value,)).copy() \
+        if nbytes.value else np.zeros(0, np.uint8)
+    secs = {}
+    width = {"entries": 4, "dunits": 8, "sunits": 8}
+    for i, name in enumerate(SEC):
+        o, n = int(off[i]), int(cnt[i])
+        k = width.get(name, 1)
+        secs[name] = blob[o:o + 4 * n * k].view(np.int32).reshape(n, k) if k > 1 else \
+            blob[o:o + 4 * n].view(np.int32)
+    return secs
+
+
+def simulate(w, tree):
+    view = tree.view()
+    P = plan_image(tree)
+    g = w.num_q_heads // w.num_kv_heads
+    D, Hq, Hkv, ps = w.head_dim, w.num_q_heads, w.num_kv_heads, w.page_size
+    pid, pcnt, phash = page_slot_hashes(w, view)
+    page_index = {int(p): i for i, p in enumerate(pid)}
+    gid, tt = query_rows(w)
+    T = len(gid)
+    Q = np.zeros((T, Hq, D))
+    for i in range(T):
+        Q[i] = V.q_values(int(gid[i]), np.array([tt[i]]), w.seed, Hq, D, w.scale_q)[0]
+    nprow = tree.plan_info()["n_partial_rows"]
+    part_o = np.full((nprow, Hq, D), np.nan)
+    part_l = np.full((nprow, Hq), np.nan)
+    out = np.full((T, Hq, D), np.nan)
+    lse = np.full((T, Hq), np.nan)
+    written = np.zeros((T, Hq), dtype=np.int64)
+    for units in (P["dunits"], P["sunits"]):
+        for u in units:
+            item, kvh, rb, nr, eb, ee, pmb, tb = (int(x) for x in u)
+            kpos, K, Vv = [], [], []
+            for e in range(eb, ee):
+                page, roff, pos0, cnt = (int(x) for x in P["entries"][e])
+                pi = page_index[page]
+                h = phash[pi * ps + roff: pi * ps + roff + cnt]
+                K.append(V.kv_values(h, w.seed, 0, Hkv, D)[:, kvh])
+                Vv.append(V.kv_values(h, w.seed, 1, Hkv, D)[:, kvh])
+                kpos.extend(range(pos0, pos0 + cnt))
+            K = np.concatenate(K)[:, None, :]
+            Vv = np.concatenate(Vv)[:, None, :]
+            for r in range(nr):
+                ir = rb + r
+                tl, j = ir // g, ir % g
+                tok = int(P["item_tokens"][tb + tl])
+                head = kvh * g + j
+                pos = int(P["tok_pos"][tok])
+                o, l = A.partial(K, Vv, Q[tok:tok + 1, head:head + 1], [pos], kpos)
+                tgt = int(P["partmap"][pmb + tl])
+                if tgt == -2:
+                    continue
+                if tgt == -1:
+                    out[tok, head], lse[tok, head] = o[0, 0], l[0, 0]
+                    written[tok, head] += 1
+                else:
+                    assert np.isnan(part_l[tgt, head]), "partial row written twice"
+                    part_o[tgt, head], part_l[tgt, head] = o[0, 0], l[0, 0]
+    mo = P["merge_off"]
+    for m, tok in enumerate(P["merge_tok"]):
+        rows = P["merge_rows"][mo[m]:mo[m + 1]]
+        assert not np.isnan(part_l[rows]).any(), "merge reads an unwritten partial"
+        O, L = A.lse_merge([(part_o[r][None], part_l[r][None]) for r in rows])
+        out[tok], lse[tok] = O[0], L[0]
+        written[tok] += 1
+    return out, lse, written, P
