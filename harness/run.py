@@ -124,3 +124,66 @@ def work_counts(w, view):
     kv = int(view["node_len"].astype(np.int64).sum()) * w.num_kv_heads * w.head_dim * 2 * b
     qo = int(q.sum()) * w.num_q_heads * w.head_dim * b * 2
     return F, kv + qo, kv
+
+
+def subset(w, reqs, name=None):
+    """Workload restricted to requests `reqs` (ascending), keeping global ids."""
+    from synth.workloads import Workload
+    reqs = np.asarray(reqs, dtype=np.int64)
+    paths = [w.path(int(r)) for r in reqs]
+    tok_off = np.zeros(len(reqs) + 1, dtype=np.int64)
+    if len(reqs):
+        tok_off[1:] = np.cumsum([len(p) for p in paths])
+    gid = np.asarray([w.gid(int(r)) for r in reqs], dtype=np.int64)
+    return Workload(name=name or w.name, seed=w.seed, num_q_heads=w.num_q_heads,
+                    num_kv_heads=w.num_kv_heads, head_dim=w.head_dim, kv_dtype=w.kv_dtype,
+                    page_size=w.page_size, model_params=w.model_params, hidden=w.hidden,
+                    layers=w.layers,
+                    tokens=np.concatenate(paths).astype(np.int32) if paths else np.zeros(0, np.int32),
+                    tok_off=tok_off, q_len=w.q_len[reqs], prompt_len=w.prompt_len[reqs],
+                    out_len=w.out_len[reqs], scale_q=w.scale_q, global_id=gid)
+
+
+def pass_work(w, view, rows_min=128, force_class=0):
+    """Algorithmic work of the two passes, mirroring the planner's item split:
+    SEPARATE-node items and BIG-request items are dense iff rows*g >= rows_min.
+    Returns dict(dense_flops, dense_bytes, stream_flops, stream_bytes) where
+    flops = 4 D x (visible (row, key) pairs) and bytes = distinct KV bytes of the
+    pass's items + Q read + O written (dtype bytes)."""
+    g = w.num_q_heads // w.num_kv_heads
+    D, Hq, Hkv = w.head_dim, w.num_q_heads, w.num_kv_heads
+    b = 2 if w.kv_dtype == "bf16" else 4
+    n = np.diff(w.tok_off)
+    ncls, rcls = view["node_class"], view["req_class"]
+    start, ln = view["node_start"], view["node_len"]
+    po, pn = view["req_path_off"], view["req_path_nodes"]
+
+    def vis(r, node):
+        a = int(n[r]) - int(w.q_len[r])
+        pos = np.arange(a, int(n[r]))
+        return int(np.clip(pos - int(start[node]) + 1, 0, int(ln[node])).sum())
+
+    sep_rows = {}
+    sep_vis = {}
+    out = dict(dense_flops=0, dense_bytes=0, stream_flops=0, stream_bytes=0)
+    for r in range(w.n_req):
+        folded_vis, folded_len = 0, 0
+        for k in range(int(po[r]), int(po[r + 1])):
+            node = int(pn[k])
+            if ncls[node] and (not rcls[r] or force_class == 1):
+                sep_rows[node] = sep_rows.get(node, 0) + int(w.q_len[r])
+                sep_vis[node] = sep_vis.get(node, 0) + vis(r, node)
+            else:
+                folded_vis += vis(r, node)
+                folded_len += int(ln[node])
+        if folded_len == 0:
+            continue
+        dense = int(w.q_len[r]) * g >= rows_min
+        key = "dense" if dense else "stream"
+        out[key + "_flops"] += 4 * D * Hq * folded_vis
+        out[key + "_bytes"] += folded_len * Hkv * D * 2 * b + 2 * int(w.q_len[r]) * Hq * D * b
+    for node, rows in sep_rows.items():
+        key = "dense" if rows * g >= rows_min else "stream"
+        out[key + "_flops"] += 4 * D * Hq * sep_vis[node]
+        out[key + "_bytes"] += int(ln[node]) * Hkv * D * 2 * b + 2 * rows * Hq * D * b
+    return out

@@ -12,6 +12,7 @@
 // are compared by exact 256-bit cross products, so results are bit-identical to
 // the Python-int oracle (oracle/tree.py), which shares no code with this file.
 #include <algorithm>
+#include <climits>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -629,7 +630,8 @@ int build_plan(blend_tree* t) {
     const int32_t tr = it.dense ? tile_d : tile_s;
     for (int64_t rb = 0; rb < rows; rb += tr) {
       int32_t nr = (int32_t)std::min<int64_t>(tr, rows - rb);
-      int32_t maxpos = tok_pos[it.toks[(rb + nr - 1) / g]];
+      int32_t maxpos = INT32_MIN;   // SEPARATE items mix requests: positions are not sorted
+      for (int64_t tl = rb / g; tl <= (rb + nr - 1) / g; ++tl) maxpos = std::max(maxpos, tok_pos[it.toks[tl]]);
       int32_t trunc = 0;   // entries with pos0 <= maxpos (ascending positions)
       while (trunc < (int32_t)it.ents.size() && it.ents[trunc].pos0 <= maxpos) ++trunc;
       for (size_t s = 0; s + 1 < split_b[ii].size(); ++s) {

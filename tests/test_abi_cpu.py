@@ -168,3 +168,14 @@ def test_plan_simulation_c2_small():
     t = _check_sim(w, rows_min=64)
     info = t.plan_info()
     assert info["n_dense_units"] > 0 and info["n_stream_units"] > 0
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_plan_simulation_mixed_sep_rows(seed):
+    """SEPARATE items mixing prefill rows of several requests (unsorted positions)."""
+    hq, hkv = [(8, 2), (32, 8), (16, 1), (4, 4)][seed % 4]
+    w = random_workload(seed, hq=hq, hkv=hkv, d=128 if seed % 2 else 64, kv_dtype="bf16",
+                        page_size=[16, 32, 64, 128][seed % 4], max_seg=200, n_req=int(6 + seed * 2),
+                        max_q=64)
+    for kw in (dict(), dict(force_class=1, min_sep_len=0), dict(rows_min=16, min_sep_len=0)):
+        _check_sim(w, **kw)
