@@ -251,6 +251,10 @@ def run_ours(args):
 
     K = args.steps
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    for row in ev:            # torch creates CUDA events lazily: materialise the handles
+        for e in row:
+            e.record(stream)
+    torch.cuda.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.2)

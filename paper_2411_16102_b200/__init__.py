@@ -100,12 +100,12 @@ EXPORTS = {
 
 
 def lib():
-    """Load libblend.so (built in-tree by paper_2411_16102_b200.build); raise if missing."""
+    """Load libblend.so (built in-tree by paper_2411_16102_b200.compile); raise if missing."""
     global _lib
     if _lib is None:
         if not os.path.exists(LIB_PATH):
             raise ImportError(f"libblend.so not built ({LIB_PATH}); run "
-                              "`python -m paper_2411_16102_b200.build` — there is no fallback")
+                              "`python -m paper_2411_16102_b200.compile` — there is no fallback")
         L = C.CDLL(LIB_PATH)
         for name, (res, args) in EXPORTS.items():
             f = getattr(L, name)

@@ -1,7 +1,7 @@
 """Build libblend.so in-tree: every .cu for sm_100a (nvcc), host.cpp (g++ via nvcc),
 cudart linked statically so the library loads on a CPU-only box too.
 
-    python -m paper_2411_16102_b200.build [--force] [--verbose]
+    python -m paper_2411_16102_b200.compile [--force] [--verbose]
 """
 from __future__ import annotations
 
