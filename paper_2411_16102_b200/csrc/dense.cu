@@ -325,6 +325,8 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       ++gu;
     }
   }
+  __syncwarp();       // lane 0 of the producer / MMA warps rejoins its warp before the CTA barrier
+  ptx::tc_fence_before();
   __syncthreads();
   if (warp == 2) {
     ptx::tc_fence_after();

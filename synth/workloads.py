@@ -161,6 +161,58 @@ def c5_70b_32k(seed: int = 5, n_docs: int = 16, per_doc: int = 64, doc_len: int 
     return _pack("c5_70b_32k", seed, paths, q, p, d, dict(LLAMA70B), "bf16", 64)
 
 
+def c4_grid(seed: int = 4, counts=(18646, 54, 21300), chunk: int = 512) -> Workload:
+    """configs[3]: the paper's A.1 grid recipe with synthetic lengths —
+    40,000 requests mixing BurstGPT-like (prompt LN(600, 0.7) in [16, 4096], output
+    LN(256, 0.7) in [1, 4096]), OpenVid-like (caption LN(100, 0.4) in [16, 512],
+    frames LN(64, 0.3) in [8, 256], d = 256 frames rescaled to mean 16384) and
+    MMLU-like requests (57 subjects with a 5-shot prefix U{400..1000}, question
+    LN(100, 0.4) in [20, 400], d = 2); 3-level tree: trace system prompt (128)
+    -> MMLU subject -> request.  Counts (Burst, OpenVid, MMLU) = SURVEY §8(d-4)'s
+    expected-length solve for compute density t = 1.0 and sharing s = 0.5.
+    Snapshot: every request sits at a uniformly random step of its lifetime
+    (ceil(p_private / 512) prefill chunks, then d decodes); shared prefixes cached."""
+    rng = np.random.default_rng(seed)
+    nb, nv, nm = counts
+    sys_b, sys_v, sys_m = _toks(rng, 128), _toks(rng, 128), _toks(rng, 128)
+    subj = [_toks(rng, int(rng.integers(400, 1001))) for _ in range(57)]
+    paths, q, p, d = [], [], [], []
+
+    def snapshot(shared, priv_len, dd):
+        n_chunks = -(-priv_len // chunk)
+        k = int(rng.integers(0, n_chunks + dd))
+        if k < n_chunks:
+            cached = min((k + 1) * chunk, priv_len)
+            qq = cached - k * chunk
+            priv = _toks(rng, cached)
+        else:
+            priv = _toks(rng, priv_len + (k - n_chunks) + 1)
+            qq = 1
+        return np.concatenate([shared, priv]), qq
+
+    pb = _lognormal_mean(rng, 600, 0.7, nb, 16, 4096)
+    db = _lognormal_mean(rng, 256, 0.7, nb, 1, 4096)
+    for i in range(nb):
+        path, qq = snapshot(sys_b, int(pb[i]), int(db[i]))
+        paths.append(path); q.append(qq); p.append(128 + int(pb[i])); d.append(int(db[i]))
+    cap = _lognormal_mean(rng, 100, 0.4, nv, 16, 512)
+    frames = _lognormal_mean(rng, 64, 0.3, nv, 8, 256)
+    dv = 256 * frames
+    dv = np.maximum(1, np.rint(dv * (16384.0 / max(1.0, dv.mean())))).astype(np.int64)
+    for i in range(nv):
+        path, qq = snapshot(sys_v, int(cap[i]), int(dv[i]))
+        paths.append(path); q.append(qq); p.append(128 + int(cap[i])); d.append(int(dv[i]))
+    qm = _lognormal_mean(rng, 100, 0.4, nm, 20, 400)
+    sm = rng.integers(0, 57, size=nm)
+    for i in range(nm):
+        shared = np.concatenate([sys_m, subj[int(sm[i])]])
+        path, qq = snapshot(shared, int(qm[i]), 2)
+        paths.append(path); q.append(qq); p.append(len(shared) + int(qm[i])); d.append(2)
+    order = rng.permutation(len(paths))             # arrival order is not tree order
+    return _pack("c4_grid_t1.0_s0.5", seed, [paths[i] for i in order], np.asarray(q)[order],
+                 np.asarray(p)[order], np.asarray(d)[order], dict(LLAMA8B), "bf16", 64)
+
+
 def concat(workloads: List[Workload], name: str) -> Workload:
     """Union of independent workloads (weak-scaling global batch).  Global ids are
     positions in the union; the union's value seed (K/V/Q generator) is the first
@@ -190,7 +242,7 @@ def by_name(name: str) -> Workload:
         "c1c": lambda: c1_tiny("c"), "c1d": lambda: c1_tiny("d"),
         "c1a_bf16": lambda: c1_tiny("a", "bf16"), "c1b_bf16": lambda: c1_tiny("b", "bf16"),
         "c1c_bf16": lambda: c1_tiny("c", "bf16"), "c1d_bf16": lambda: c1_tiny("d", "bf16"),
-        "c2": c2_mmlu_decode, "c3": c3_burst_openvid, "c5": c5_70b_32k,
+        "c2": c2_mmlu_decode, "c3": c3_burst_openvid, "c4": c4_grid, "c5": c5_70b_32k,
     }
     return table[name]()
 
