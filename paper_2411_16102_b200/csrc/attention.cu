@@ -12,6 +12,7 @@ extern "C" int blend_internal_plan_image(const blend_tree* t, const void** data,
                                          const int64_t** count);
 extern "C" int blend_internal_tree_dims(const blend_tree* t, int32_t* dims);
 extern "C" int64_t blend_internal_partial_rows(const blend_tree* t);
+extern "C" int64_t blend_internal_stream_entries(const blend_tree* t);
 
 namespace blend {
 cudaError_t launch_generic(const AttnParams& p, cudaStream_t st);
@@ -50,6 +51,7 @@ extern "C" int blend_plan_upload(const blend_tree* tree, void* dev_buf, size_t b
     plan->count[i] = count[i];
   }
   plan->count[blend::SEC_COUNT] = blend_internal_partial_rows(tree);
+  plan->count[blend::SEC_COUNT + 1] = blend_internal_stream_entries(tree);
   int32_t dims[5];
   blend_internal_tree_dims(tree, dims);
   plan->num_q_heads = dims[0];
@@ -119,6 +121,7 @@ extern "C" int blend_attention(const blend_attn_args* a, void* stream) {
   AttnParams ps_ = p;
   ps_.units = (const Unit*)(base + pl.off[SEC_STREAM_UNITS]);
   ps_.n_units = (int32_t)pl.count[SEC_STREAM_UNITS];
+  ps_.avg_entries = ps_.n_units > 0 ? (int32_t)(pl.count[SEC_COUNT + 1] / ps_.n_units) : 0;
   if (generic) e = launch_generic(ps_, st);
   else e = launch_stream(ps_, a->n_cache_pages, st);
   if (e != cudaSuccess) return cuda_fail(e);

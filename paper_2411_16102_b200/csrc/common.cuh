@@ -33,6 +33,7 @@ struct AttnParams {
   int32_t hq, hkv, g, d, ps;
   int32_t kv_f32;   // 1: fp32 q/k/v/out, 0: bf16
   float scale_log2; // log2(e) / sqrt(D)
+  int32_t avg_entries;   // host-side launch heuristic: mean entries per unit
 };
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {

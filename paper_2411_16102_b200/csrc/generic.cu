@@ -131,29 +131,44 @@ __global__ void __launch_bounds__(128) generic_unit_kernel(AttnParams p) {
   }
 }
 
-// One CTA per merged token; threads stride over (head, element).
+// One warp per (merged token, q head); lanes own D/32 contiguous elements.
 __global__ void __launch_bounds__(256) merge_kernel(AttnParams p) {
   const int m = blockIdx.x;
+  const int h = blockIdx.y * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (h >= p.hq) return;
   const int token = p.merge_tok[m];
   const int s0 = p.merge_off[m], s1 = p.merge_off[m + 1];
   const int D = p.d;
-  for (int idx = threadIdx.x; idx < p.hq * D; idx += blockDim.x) {
-    const int h = idx / D, e = idx % D;
-    float mx = -INFINITY;
-    for (int s = s0; s < s1; ++s) mx = fmaxf(mx, p.ws_lse[(int64_t)p.merge_rows[s] * p.hq + h]);
-    float o = 0.f, tot = 0.f;
-    if (mx != -INFINITY) {
-      for (int s = s0; s < s1; ++s) {
-        const int64_t row = p.merge_rows[s];
-        float w = exp2f(p.ws_lse[row * p.hq + h] - mx);
-        tot += w;
-        o = fmaf(w, p.ws_o[(row * p.hq + h) * D + e], o);
+  const int vec = D / 32;          // 2 or 4 elements per lane
+  const int e0 = lane * vec;
+  float mx = -INFINITY;
+  for (int s = s0; s < s1; ++s) mx = fmaxf(mx, p.ws_lse[(int64_t)p.merge_rows[s] * p.hq + h]);
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  float tot = 0.f;
+  if (mx != -INFINITY) {
+    for (int s = s0; s < s1; ++s) {
+      const int64_t row = p.merge_rows[s];
+      const float w = exp2f(p.ws_lse[row * p.hq + h] - mx);
+      tot += w;
+      const float* src = p.ws_o + (row * p.hq + h) * D + e0;
+      if (vec == 4) {
+        const float4 v = *reinterpret_cast<const float4*>(src);
+        acc[0] = fmaf(w, v.x, acc[0]);
+        acc[1] = fmaf(w, v.y, acc[1]);
+        acc[2] = fmaf(w, v.z, acc[2]);
+        acc[3] = fmaf(w, v.w, acc[3]);
+      } else {
+        const float2 v = *reinterpret_cast<const float2*>(src);
+        acc[0] = fmaf(w, v.x, acc[0]);
+        acc[1] = fmaf(w, v.y, acc[1]);
       }
-      o /= tot;
     }
-    st_elem(p.out, ((int64_t)token * p.hq + h) * D + e, o, p.kv_f32);
-    if (e == 0) p.lse[(int64_t)token * p.hq + h] = mx != -INFINITY ? (mx + log2f(tot)) * kLn2 : -INFINITY;
   }
+  const float inv = tot > 0.f ? 1.f / tot : 0.f;
+  const int64_t ob = ((int64_t)token * p.hq + h) * D + e0;
+  for (int k = 0; k < vec; ++k) st_elem(p.out, ob + k, acc[k] * inv, p.kv_f32);
+  if (lane == 0) p.lse[(int64_t)token * p.hq + h] = mx != -INFINITY ? (mx + log2f(tot)) * kLn2 : -INFINITY;
 }
 
 size_t generic_smem_bytes(int D) {
@@ -172,7 +187,7 @@ cudaError_t launch_generic(const AttnParams& p, cudaStream_t st) {
 
 cudaError_t launch_merge(const AttnParams& p, cudaStream_t st) {
   if (p.n_merge <= 0) return cudaSuccess;
-  merge_kernel<<<p.n_merge, 256, 0, st>>>(p);
+  merge_kernel<<<dim3(p.n_merge, (p.hq + 7) / 8), 256, 0, st>>>(p);
   return cudaPeekAtLastError();
 }
 

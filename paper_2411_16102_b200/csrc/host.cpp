@@ -100,6 +100,7 @@ struct blend_tree {
   blend_plan_info info{};
   size_t workspace_bytes = 0;
   int64_t n_partial_rows = 0;
+  int64_t stream_entries = 0;   // sum over stream units of their entry counts (launch heuristic)
 };
 
 namespace {
@@ -527,8 +528,9 @@ int build_plan(blend_tree* t) {
     chunk_s = std::max<int64_t>(512, (work_s + 8LL * num_sms - 1) / (8LL * num_sms));
     chunk_s = (chunk_s + 63) / 64 * 64;
   }
+  // dense split-KV: fill (at most) one wave of persistent CTAs without exceeding it
   int64_t dsplit = 1;
-  if (base_d > 0 && base_d < 2LL * num_sms) dsplit = (2LL * num_sms + base_d - 1) / base_d;
+  if (base_d > 0 && base_d < num_sms) dsplit = num_sms / base_d;
 
   std::vector<std::vector<int32_t>> split_b(items.size());   // entry boundaries per item
   for (size_t ii = 0; ii < items.size(); ++ii) {
@@ -653,6 +655,8 @@ int build_plan(blend_tree* t) {
   };
   std::stable_sort(dunits.begin(), dunits.end(), by_work);
   std::stable_sort(sunits.begin(), sunits.end(), by_work);
+  t->stream_entries = 0;
+  for (const auto& u : sunits) t->stream_entries += u.entry_end - u.entry_begin;
 
   std::vector<int32_t> item_tokens(item_tok_off.back());
   for (size_t ii = 0; ii < items.size(); ++ii)
@@ -919,6 +923,7 @@ int blend_internal_plan_image(const blend_tree* t, const void** data, size_t* by
 int blend_internal_fail(int status, const char* msg) { return fail(status, "%s", msg); }
 
 int64_t blend_internal_partial_rows(const blend_tree* t) { return t ? t->n_partial_rows : 0; }
+int64_t blend_internal_stream_entries(const blend_tree* t) { return t ? t->stream_entries : 0; }
 
 int blend_internal_tree_dims(const blend_tree* t, int32_t* dims) {
   if (!t) return fail(BLEND_EINVAL, "tree is NULL");

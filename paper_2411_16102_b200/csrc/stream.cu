@@ -48,7 +48,7 @@ __host__ __device__ inline StreamSmem stream_smem_layout(int D, int nstage) {
 }
 
 template <int D>
-__global__ void __launch_bounds__(ST_THREADS, 1)
+__global__ void __launch_bounds__(ST_THREADS, 2)
     stream_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv, AttnParams p,
                   int nstage, int box_rows) {
   constexpr int CH = D / 64;       // 128-B chunks per row
@@ -357,12 +357,19 @@ static cudaError_t launch_stream_d(const AttnParams& p, int64_t n_cache_pages, c
   if (e != cudaSuccess) return e;
   e = make_cache_tmap(&tv, p.v_cache, rows, D, box_rows);
   if (e != cudaSuccess) return e;
-  int nstage = 6;
-  while (nstage > 2 && stream_smem_layout(D, nstage).total + 1024 > 227 * 1024) --nstage;
+  // Short units (decode over a ~100-token private suffix): 2 CTAs per SM with a 2-stage
+  // ring each, so one CTA's per-unit prologue/epilogue overlaps the other's streaming.
+  // Long units (16K-token contexts): 1 CTA per SM with the deepest ring that fits.
+  const int64_t avg_entries = p.avg_entries;
+  int ctas_per_sm = avg_entries <= 8 ? 2 : 1;
+  int nstage = ctas_per_sm == 2 ? 2 : 6;
+  const int budget = ctas_per_sm == 2 ? 113 * 1024 : 227 * 1024;
+  while (nstage > 2 && (int)stream_smem_layout(D, nstage).total + 1024 > budget) --nstage;
   const size_t smem = stream_smem_layout(D, nstage).total + 1024;
   e = cudaFuncSetAttribute(stream_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const int grid = p.n_units < num_sms_cached() ? p.n_units : num_sms_cached();
+  const int slots = ctas_per_sm * num_sms_cached();
+  const int grid = p.n_units < slots ? p.n_units : slots;
   stream_kernel<D><<<grid, ST_THREADS, smem, st>>>(tk, tv, p, nstage, box_rows);
   return cudaPeekAtLastError();
 }
