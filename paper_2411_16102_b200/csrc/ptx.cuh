@@ -170,3 +170,16 @@ __device__ __forceinline__ float ex2(float x) {
 }
 }  // namespace ptx
 }  // namespace blend
+
+namespace blend {
+namespace ptx {
+// D[tmem] (+)= A[tmem] * B[smem desc]: A (M x 16, bf16 pairs packed per 32-bit column) read from TMEM
+__device__ __forceinline__ void umma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+}  // namespace ptx
+}  // namespace blend

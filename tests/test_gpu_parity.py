@@ -147,7 +147,7 @@ def test_page_permutation_and_classes_invariance():
     assert (db3.out.float() - db4.out.float()).abs().max().item() < 2e-2
 
 
-@pytest.mark.parametrize("name", ["c3", "c5"])
+@pytest.mark.parametrize("name", ["c3", "c4", "c5"])
 def test_large_configs_sampled(name):
     """Full-size C3 / C5 in the bench's launch configuration, checked on a
     stratified request sample (BIG/SMALL, shortest/longest contexts)."""
@@ -163,3 +163,33 @@ def test_large_configs_sampled(name):
     rng = np.random.default_rng(0)
     pick |= set(rng.choice(w.n_req, size=6, replace=False).tolist())
     _cmp(w, db, sorted(pick))
+
+
+def test_request_order_invariance():
+    """Permuting the caller's request order leaves every request's rows bitwise equal
+    (each row's arithmetic does not depend on which other rows share its tile)."""
+    from harness.run import subset
+    w = W.c2_mmlu_decode(n_req=48)
+    db = device_batch(w)
+    db.run()
+    perm = np.random.default_rng(3).permutation(w.n_req)
+    w2 = subset(w, perm)                      # global ids travel with the requests
+    db2 = device_batch(w2)
+    db2.run()
+    torch.cuda.synchronize()
+    a, b = db.out.cpu(), db2.out.cpu()
+    for i, r in enumerate(perm):
+        assert torch.equal(a[r], b[i]), r
+
+
+def test_abi_errors():
+    w = W.c1_tiny("a", "bf16")
+    db = device_batch(w, tree_kw=dict(force_class=1, min_sep_len=0))
+    with pytest.raises(B.BlendError) as e:
+        B.attention(db.q, db.k_cache, db.v_cache, db.plan, db.out, db.lse, db.ws[:16],
+                    n_cache_pages=db.n_cache_pages)
+    assert e.value.status == B.ENOSPC
+    with pytest.raises(B.BlendError) as e:
+        B.attention(db.q, db.k_cache, db.v_cache, db.plan, db.out, db.lse, db.ws,
+                    n_cache_pages=db.n_cache_pages, path=7)
+    assert e.value.status == B.EINVAL
