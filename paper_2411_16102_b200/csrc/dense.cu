@@ -3,20 +3,25 @@
 // Work units with many rows per kv head — a SEPARATE shared-prefix node attended
 // once by all the SMALL requests under it (PAPER §5 P:11 "exactly-once computation
 // of shared prefixes"; §7.2 P:248-251 cascade reuse of the shared KV access), or a
-// BIG request (chunked prefill) — are dense contractions: 128 query rows
-// (tokens x grouped q heads) against 128-key blocks of the node's pages.
+// BIG request (chunked prefill) — are dense contractions: up to 256 query
+// rows (tokens x grouped q heads) against 128-key blocks of the node's pages.
 //
-// One persistent CTA per SM, warp-specialised:
-//   warp 0      TMA producer: K/V page entries (128B swizzle) -> 2-stage smem ring
-//   warp 1      MMA issuer (one thread): S = Q K^T (UMMA 128x128x16, K-major A/B)
-//               into a double-buffered TMEM S; O += P V (P K-major from smem, V
-//               MN-major) into TMEM O; tcgen05.commit -> mbarriers
-//   warp 2      TMEM allocator (512 columns: S0 | S1 | O)
-//   warps 4..7  softmax / epilogue: thread = query row = TMEM lane.  tcgen05.ld the
-//               S row, per-row causal mask, log2-domain online softmax with lazy
-//               O rescaling (only when the running max grows by > 8), P -> bf16
-//               smem (128B swizzle), final O / l -> bf16 row or fp32 partial.
-// QK_{j+1} runs on the tensor pipe while the softmax of block j runs.
+// One persistent CTA per SM, warp-specialised, two 128-row Q tiles (A, B) that
+// share every K/V block ("ping-pong": the tensor pipe works on one tile while the
+// other tile's softmax runs):
+//   warp 0       TMA producer: K/V page entries (128B swizzle) -> smem stage ring
+//   warp 1       MMA issuer (one thread): S_t = Q_t K^T (UMMA 128x128x16, K-major
+//                A/B from smem) into TMEM; O_t += P_t V with P_t read from TMEM
+//                (aliasing S_t) and V MN-major from smem; tcgen05.commit -> mbarriers
+//   warp 2       TMEM allocator (512 columns: S_A | S_B | O_A | O_B)
+//   warps 4..7   softmax / epilogue of tile A, warps 8..11 of tile B: thread =
+//                query row = TMEM lane; tcgen05.ld the S row, per-row causal mask,
+//                log2-domain online softmax with lazy O rescaling (only when the
+//                running max grows by > 8), P -> bf16 -> tcgen05.st into TMEM,
+//                final O / l -> bf16 row or fp32 partial.
+// MMAs of one thread execute in issue order, so QK_t(j+1) (which overwrites S_t
+// and hence P_t) is issued right after PV_t(j) without a further barrier, and the
+// commit after QK_t(j+1) also certifies PV_t(j) (the softmax may then rescale O_t).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <math.h>
@@ -27,23 +32,23 @@
 
 namespace blend {
 
-constexpr int DN_THREADS = 256;
+constexpr int DN_THREADS = 384;
 constexpr int DN_KB = 128;               // keys per block (UMMA N of QK^T, K of PV)
 constexpr int DN_CHUNK = 128 * 128;      // 128 rows x 128 B (one 64-column chunk)
 constexpr uint32_t DN_TMEM_COLS = 512;
 constexpr float DN_RESCALE_T = 8.0f;     // lazy-rescale threshold (log2 units)
 
 struct DenseSmem {
-  uint32_t q, p, stage0, stage_stride, bar, total;
+  uint32_t q0, q1, stage0, stage_stride, bar, total;
   int nstage;
 };
 
 __host__ __device__ inline DenseSmem dense_layout(int D) {
   DenseSmem L;
   const int CH = D / 64;
-  L.q = 0;
-  L.p = CH * DN_CHUNK;
-  L.stage0 = L.p + 2 * DN_CHUNK;
+  L.q0 = 0;
+  L.q1 = CH * DN_CHUNK;
+  L.stage0 = 2 * CH * DN_CHUNK;
   L.stage_stride = 2 * CH * DN_CHUNK;
   L.nstage = D == 128 ? 2 : 4;
   L.bar = L.stage0 + L.nstage * L.stage_stride;
@@ -61,14 +66,14 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
   const DenseSmem L = dense_layout(D);
   const int NS = L.nstage;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar);
-  uint64_t* kv_full = bars;            // [NS]
+  uint64_t* kv_full = bars;            // [NS <= 4]
   uint64_t* kv_empty = bars + 4;       // [NS]
-  uint64_t* s_full = bars + 8;         // [2]
-  uint64_t* q_full = bars + 10;
-  uint64_t* q_empty = bars + 11;
-  uint64_t* p_full = bars + 12;
-  uint64_t* o_done = bars + 13;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  uint64_t* s_full = bars + 8;         // [2] per tile
+  uint64_t* p_full = bars + 10;        // [2]
+  uint64_t* o_done = bars + 12;        // [2]
+  uint64_t* q_full = bars + 14;        // [2]
+  uint64_t* q_empty = bars + 16;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -76,12 +81,13 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       ptx::mbar_init(&kv_full[s], 1);
       ptx::mbar_init(&kv_empty[s], 1);
     }
-    ptx::mbar_init(&s_full[0], 1);
-    ptx::mbar_init(&s_full[1], 1);
-    ptx::mbar_init(q_full, 4);
+    for (int t = 0; t < 2; ++t) {
+      ptx::mbar_init(&s_full[t], 1);
+      ptx::mbar_init(&p_full[t], 4);
+      ptx::mbar_init(&o_done[t], 1);
+      ptx::mbar_init(&q_full[t], 4);
+    }
     ptx::mbar_init(q_empty, 1);
-    ptx::mbar_init(p_full, 4);
-    ptx::mbar_init(o_done, 1);
     ptx::fence_mbar_init();
   }
   if (warp == 2) ptx::tmem_alloc(tmem_slot, DN_TMEM_COLS);
@@ -98,8 +104,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       uint32_t kit = 0;
       for (int ui = blockIdx.x; ui < p.n_units; ui += gridDim.x) {
         const Unit u = p.units[ui];
-        const int ne = u.entry_end - u.entry_begin;
-        const int nb = (ne + EPB - 1) / EPB;
+        const int nb = (u.entry_end - u.entry_begin + EPB - 1) / EPB;
         for (int j = 0; j < nb; ++j, ++kit) {
           const uint32_t s = kit % NS, ph = (kit / NS) & 1;
           ptx::mbar_wait(&kv_empty[s], ph ^ 1);
@@ -126,89 +131,108 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
     if (lane == 0) {
       constexpr uint32_t IDESC_QK = ptx::umma_idesc_bf16(128, DN_KB, 0, 0);
       constexpr uint32_t IDESC_PV = ptx::umma_idesc_bf16(128, D, 0, 1);
-      const uint32_t q_addr = ptx::smem_u32(smem + L.q);
-      const uint32_t p_addr = ptx::smem_u32(smem + L.p);
-      uint32_t kit = 0, gb = 0, gu = 0;
+      const uint32_t q_addr0 = ptx::smem_u32(smem + L.q0), q_addr1 = ptx::smem_u32(smem + L.q1);
+      uint32_t kit = 0, gu = 0, pb0 = 0, pb1 = 0;
       for (int ui = blockIdx.x; ui < p.n_units; ui += gridDim.x) {
         const Unit u = p.units[ui];
         const int nb = (u.entry_end - u.entry_begin + EPB - 1) / EPB;
-        ptx::mbar_wait(q_full, gu & 1);
+        const int ntile = u.n_rows > 128 ? 2 : 1;
+        ptx::mbar_wait(&q_full[0], gu & 1);
+        ptx::mbar_wait(&q_full[1], gu & 1);
         ptx::tc_fence_after();
-        for (int j = 0; j <= nb; ++j) {
-          if (j < nb) {
-            const uint32_t s = (kit + j) % NS;
-            ptx::mbar_wait(&kv_full[s], ((kit + j) / NS) & 1);
-            ptx::tc_fence_after();
-            const uint32_t kst = ptx::smem_u32(smem + L.stage0 + s * L.stage_stride);
-            const uint32_t sb = (gb + j) & 1;
+        uint32_t s = kit % NS;
+        ptx::mbar_wait(&kv_full[s], (kit / NS) & 1);
+        ptx::tc_fence_after();
+        uint32_t kst = ptx::smem_u32(smem + L.stage0 + s * L.stage_stride);
+        for (int t = 0; t < ntile; ++t) {
+          const uint32_t qa = t ? q_addr1 : q_addr0;
 #pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk) {
-              const uint32_t off = (kk / 4) * DN_CHUNK + (kk % 4) * 32;
-              ptx::umma_f16(tmem + sb * DN_KB, ptx::umma_desc_sw128(q_addr + off, 16, 1024),
-                            ptx::umma_desc_sw128(kst + off, 16, 1024), IDESC_QK, kk > 0);
-            }
-            ptx::umma_commit(&s_full[sb]);
-            if (j == nb - 1) ptx::umma_commit(q_empty);
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = (kk / 4) * DN_CHUNK + (kk % 4) * 32;
+            ptx::umma_f16(tmem + t * DN_KB, ptx::umma_desc_sw128(qa + off, 16, 1024),
+                          ptx::umma_desc_sw128(kst + off, 16, 1024), IDESC_QK, kk > 0);
           }
-          if (j >= 1) {
-            const int jj = j - 1;
-            const uint32_t s = (kit + jj) % NS;
-            ptx::mbar_wait(p_full, (gb + jj) & 1);
-            ptx::tc_fence_after();
-            const uint32_t vst = ptx::smem_u32(smem + L.stage0 + s * L.stage_stride) + CH * DN_CHUNK;
-#pragma unroll
-            for (int kk = 0; kk < DN_KB / 16; ++kk) {
-              const uint32_t aoff = (kk / 4) * DN_CHUNK + (kk % 4) * 32;
-              ptx::umma_f16(tmem + 2 * DN_KB, ptx::umma_desc_sw128(p_addr + aoff, 16, 1024),
-                            ptx::umma_desc_sw128(vst + kk * 16 * 128, DN_CHUNK, 1024), IDESC_PV,
-                            (jj > 0 || kk > 0) ? 1u : 0u);
-            }
-            ptx::umma_commit(&kv_empty[s]);
-            ptx::umma_commit(o_done);
-          }
+          ptx::umma_commit(&s_full[t]);
         }
+        for (int j = 0; j < nb; ++j) {
+          const uint32_t vst = kst + CH * DN_CHUNK;
+          const uint32_t s_cur = s;
+          uint32_t kst_next = 0;
+          if (j + 1 < nb) {
+            s = (kit + j + 1) % NS;
+            ptx::mbar_wait(&kv_full[s], ((kit + j + 1) / NS) & 1);
+            kst_next = ptx::smem_u32(smem + L.stage0 + s * L.stage_stride);
+          }
+          for (int t = 0; t < ntile; ++t) {
+            if (t == 0) ptx::mbar_wait(&p_full[0], (pb0++) & 1);
+            else ptx::mbar_wait(&p_full[1], (pb1++) & 1);
+            ptx::tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < DN_KB / 16; ++kk)
+              ptx::umma_f16_ts(tmem + 2 * DN_KB + t * D, tmem + t * DN_KB + kk * 8,
+                               ptx::umma_desc_sw128(vst + kk * 16 * 128, DN_CHUNK, 1024), IDESC_PV,
+                               (j > 0 || kk > 0) ? 1u : 0u);
+            if (j + 1 < nb) {
+              const uint32_t qa = t ? q_addr1 : q_addr0;
+#pragma unroll
+              for (int kk = 0; kk < D / 16; ++kk) {
+                const uint32_t off = (kk / 4) * DN_CHUNK + (kk % 4) * 32;
+                ptx::umma_f16(tmem + t * DN_KB, ptx::umma_desc_sw128(qa + off, 16, 1024),
+                              ptx::umma_desc_sw128(kst_next + off, 16, 1024), IDESC_QK, kk > 0);
+              }
+              ptx::umma_commit(&s_full[t]);
+            } else {
+              ptx::umma_commit(&o_done[t]);
+            }
+          }
+          ptx::umma_commit(&kv_empty[s_cur]);
+          kst = kst_next;
+        }
+        ptx::umma_commit(q_empty);
         kit += nb;
-        gb += nb;
         ++gu;
       }
     }
   } else if (warp >= 4) {
-    // ===================== softmax / epilogue =====================
-    const int r = threadIdx.x - 128;                 // query row = TMEM lane
-    const uint32_t lane_base = (uint32_t)((warp - 4) * 32) << 16;
-    uint8_t* qs = smem + L.q;
-    uint8_t* ps_ = smem + L.p;
-    uint32_t gb = 0, gu = 0;
+    // ===================== softmax / epilogue (tile t) =====================
+    const int t = (warp - 4) >> 2;                    // 0 = tile A, 1 = tile B
+    const int r = threadIdx.x - 128 - 128 * t;        // row within the tile = TMEM lane
+    const uint32_t lane_base = (uint32_t)(((warp - 4) & 3) * 32) << 16;
+    const uint32_t col_s = t * DN_KB, col_o = 2 * DN_KB + t * D;
+    uint8_t* qs = smem + (t ? L.q1 : L.q0);
+    uint32_t gu = 0, sb = 0, uo = 0;                  // unit, block and tile-unit counters
     for (int ui = blockIdx.x; ui < p.n_units; ui += gridDim.x) {
       const Unit u = p.units[ui];
       const int nb = (u.entry_end - u.entry_begin + EPB - 1) / EPB;
+      const bool active = t == 0 || u.n_rows > 128;
+      const int row = 128 * t + r;                    // row within the unit
       int32_t pos = INT32_MIN, token = 0, head = 0, tgt = PM_SKIP;
-      if (r < u.n_rows) {
-        RowInfo ri = row_info(p, u, r);
+      if (row < u.n_rows) {
+        RowInfo ri = row_info(p, u, row);
         pos = p.tok_pos[ri.token];
         token = ri.token;
         head = ri.head;
         tgt = row_target(p, u, ri.tl);
       }
-      // ---- Q row -> smem (K-major, 128B swizzle); wait until the previous unit's QKs are done
+      // ---- Q row -> smem (K-major, 128B swizzle) once the previous unit's MMAs are done
       if (gu > 0) ptx::mbar_wait(q_empty, (gu - 1) & 1);
-      {
+      if (active) {
         const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(p.q) +
                                                           ((int64_t)token * p.hq + head) * D);
 #pragma unroll
         for (int c = 0; c < D / 8; ++c) {
-          uint4 v = r < u.n_rows ? __ldg(src + c) : make_uint4(0, 0, 0, 0);
+          uint4 v = row < u.n_rows ? __ldg(src + c) : make_uint4(0, 0, 0, 0);
           *reinterpret_cast<uint4*>(qs + (c / 8) * DN_CHUNK + ptx::sw128(r, c % 8)) = v;
         }
+        ptx::fence_proxy_async_smem();
       }
-      ptx::fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(q_full);
+      if (lane == 0) ptx::mbar_arrive(&q_full[t]);
+      ++gu;
+      if (!active) continue;
 
       float m_ref = -INFINITY, l = 0.f;
-      for (int j = 0; j < nb; ++j) {
-        const uint32_t blk = gb + j, sb = blk & 1;
-        // visible slots per entry of this block for this row
+      for (int j = 0; j < nb; ++j, ++sb) {
         int vis[EPB];
         bool full_vis = true;
 #pragma unroll
@@ -223,41 +247,36 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
           vis[i] = v;
           full_vis = full_vis && (v == BOX);
         }
-        ptx::mbar_wait(&s_full[sb], (blk >> 1) & 1);
+        ptx::mbar_wait(&s_full[t], sb & 1);
         ptx::tc_fence_after();
-        float s[DN_KB];
-#pragma unroll
-        for (int c = 0; c < DN_KB / 32; ++c)
-          ptx::tmem_ld32(tmem + lane_base + sb * DN_KB + c * 32, reinterpret_cast<uint32_t*>(s + c * 32));
-        ptx::tmem_wait_ld();
+        // pass 1: row max over the 128 scores (32-column chunks keep registers low)
         float mx = -INFINITY;
-        if (full_vis) {
 #pragma unroll
-          for (int k = 0; k < DN_KB; ++k) mx = fmaxf(mx, s[k]);
-        } else {
+        for (int h = 0; h < 4; ++h) {
+          float sv[32];
+          ptx::tmem_ld32(tmem + lane_base + col_s + h * 32, reinterpret_cast<uint32_t*>(sv));
+          ptx::tmem_wait_ld();
 #pragma unroll
-          for (int k = 0; k < DN_KB; ++k) {
-            s[k] = (k % BOX) < vis[k / BOX] ? s[k] : -INFINITY;
-            mx = fmaxf(mx, s[k]);
+          for (int k = 0; k < 32; ++k) {
+            const int key = h * 32 + k;
+            const bool ok = full_vis || (key % BOX) < vis[key / BOX];
+            mx = fmaxf(mx, ok ? sv[k] : -INFINITY);
           }
         }
         const float mx2 = mx * p.scale_log2;
-        // PV of the previous block must be done before P smem / O are touched
-        if (j > 0) ptx::mbar_wait(o_done, (blk - 1) & 1);
         const bool need = mx2 > m_ref + DN_RESCALE_T;
+        // s_full(j) certifies PV(j-1): O may be rescaled now
         if (j > 0 && __any_sync(0xffffffffu, need)) {
-          ptx::tc_fence_after();
           const float alpha = need ? ptx::ex2(m_ref - mx2) : 1.f;
 #pragma unroll 1
           for (int c = 0; c < D / 32; ++c) {
             uint32_t ov[32];
-            ptx::tmem_ld32(tmem + lane_base + 2 * DN_KB + c * 32, ov);
+            ptx::tmem_ld32(tmem + lane_base + col_o + c * 32, ov);
             ptx::tmem_wait_ld();
 #pragma unroll
             for (int k = 0; k < 32; ++k) ov[k] = __float_as_uint(__uint_as_float(ov[k]) * alpha);
-            ptx::tmem_st32(tmem + lane_base + 2 * DN_KB + c * 32, ov);
+            ptx::tmem_st32(tmem + lane_base + col_o + c * 32, ov);
           }
-          ptx::tmem_wait_st();
         }
         if (need) {
           l *= ptx::ex2(m_ref - mx2);   // m_ref = -inf -> 0
@@ -265,30 +284,35 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         }
         const float m_use = m_ref == -INFINITY ? 0.f : m_ref;
         float lsum = 0.f;
+        // pass 2: P = exp2(s*scale - m) -> bf16 pairs -> TMEM columns [0, 64) (aliasing
+        // the already-consumed first half of S)
 #pragma unroll
-        for (int c = 0; c < DN_KB / 8; ++c) {
-          float pv[8];
+        for (int h = 0; h < 4; ++h) {
+          float sv[32];
+          ptx::tmem_ld32(tmem + lane_base + col_s + h * 32, reinterpret_cast<uint32_t*>(sv));
+          ptx::tmem_wait_ld();
+          uint32_t pk[16];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            pv[k] = ptx::ex2(fmaf(s[c * 8 + k], p.scale_log2, -m_use));
-            lsum += pv[k];
+          for (int k = 0; k < 16; ++k) {
+            const int key = h * 32 + 2 * k;
+            const bool ok0 = full_vis || (key % BOX) < vis[key / BOX];
+            const bool ok1 = full_vis || ((key + 1) % BOX) < vis[(key + 1) / BOX];
+            const float p0 = ok0 ? ptx::ex2(fmaf(sv[2 * k], p.scale_log2, -m_use)) : 0.f;
+            const float p1 = ok1 ? ptx::ex2(fmaf(sv[2 * k + 1], p.scale_log2, -m_use)) : 0.f;
+            lsum += p0 + p1;
+            pk[k] = ptx::pack_bf16(p0, p1);
           }
-          uint4 w;
-          w.x = ptx::pack_bf16(pv[0], pv[1]);
-          w.y = ptx::pack_bf16(pv[2], pv[3]);
-          w.z = ptx::pack_bf16(pv[4], pv[5]);
-          w.w = ptx::pack_bf16(pv[6], pv[7]);
-          *reinterpret_cast<uint4*>(ps_ + (c / 8) * DN_CHUNK + ptx::sw128(r, c % 8)) = w;
+          ptx::tmem_st16(tmem + lane_base + col_s + h * 16, pk);   // keys 32h.. -> columns 16h..
         }
         l += lsum;
-        ptx::fence_proxy_async_smem();
+        ptx::tmem_wait_st();
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(p_full);
+        if (lane == 0) ptx::mbar_arrive(&p_full[t]);
       }
       // ---- epilogue
-      const uint32_t last = gb + nb - 1;
-      ptx::mbar_wait(o_done, last & 1);
+      ptx::mbar_wait(&o_done[t], uo & 1);
+      ++uo;
       ptx::tc_fence_after();
       const float m_use = m_ref == -INFINITY ? 0.f : m_ref;
       const float inv = l > 0.f ? 1.f / l : 0.f;
@@ -296,7 +320,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
 #pragma unroll 1
       for (int c = 0; c < D / 32; ++c) {
         uint32_t ov[32];
-        ptx::tmem_ld32(tmem + lane_base + 2 * DN_KB + c * 32, ov);
+        ptx::tmem_ld32(tmem + lane_base + col_o + c * 32, ov);
         ptx::tmem_wait_ld();
         if (tgt == PM_DIRECT) {
           uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.out) +
@@ -321,8 +345,6 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       if (tgt == PM_DIRECT) p.lse[(int64_t)token * p.hq + head] = lse2 * kLn2;
       else if (tgt >= 0) p.ws_lse[(int64_t)tgt * p.hq + head] = lse2;
       ptx::tc_fence_before();
-      gb += nb;
-      ++gu;
     }
   }
   __syncwarp();       // lane 0 of the producer / MMA warps rejoins its warp before the CTA barrier

@@ -52,9 +52,15 @@ __global__ void __launch_bounds__(128) generic_unit_kernel(AttnParams p) {
   float* arow = lrow + GEN_ROWS;
   int* prow = reinterpret_cast<int*>(arow + GEN_ROWS);
 
-  const Unit u = p.units[blockIdx.x];
+  const Unit u0 = p.units[blockIdx.x];
+  // units carry up to 256 rows (two dense tiles): process them 128 rows at a time
+  for (int rc = 0; rc < u0.n_rows; rc += GEN_ROWS) {
+  Unit u = u0;
+  u.row_begin = u0.row_begin + rc;
+  u.n_rows = min(GEN_ROWS, u0.n_rows - rc);
   const int nr = u.n_rows;
   const int tid = threadIdx.x;
+  __syncthreads();
   for (int idx = tid; idx < nr * D; idx += blockDim.x) {
     int r = idx / D, e = idx % D;
     RowInfo ri = row_info(p, u, r);
@@ -128,6 +134,7 @@ __global__ void __launch_bounds__(128) generic_unit_kernel(AttnParams p) {
     float lse2 = l > 0.f ? mrow[r] + log2f(l) : -INFINITY;
     float inv = l > 0.f ? 1.f / l : 0.f;
     write_row(p, ri, tgt, os + r * D, inv, lse2, 32, lane);
+  }
   }
 }
 

@@ -45,7 +45,7 @@ struct Unit {
   int32_t tok_base;    // item_tok_off[item]
 };
 
-constexpr int DENSE_ROWS = 128;    // rows per dense (tcgen05, UMMA M=128) unit
+constexpr int DENSE_ROWS = 256;    // rows per dense unit: two 128-row tcgen05 Q tiles (UMMA M=128)
 constexpr int STREAM_ROWS = 16;    // rows per streaming (mma.sync m16) unit
 constexpr int ENTRY_MAX = 64;      // slots per KV entry (TMA box rows)
 
