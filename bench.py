@@ -225,7 +225,8 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     B.lib()
     path = {"auto": B.PATH_AUTO, "generic": B.PATH_GENERIC, "no_tcgen05": B.PATH_NO_TCGEN05}[args.path]
-    tree_kw = dict(num_sms=torch.cuda.get_device_properties(local).multi_processor_count)
+    tree_kw = dict(num_sms=torch.cuda.get_device_properties(local).multi_processor_count,
+                   dense_split=args.dense_split, split_tokens=args.split_tokens)
 
     gw = make_workload(args.workload, world)
     t0 = time.perf_counter()
@@ -393,6 +394,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--path", default="auto", choices=["auto", "generic", "no_tcgen05"])
     ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--dense-split", type=int, default=0, help="dense split-KV factor (0 = planner auto)")
+    ap.add_argument("--split-tokens", type=int, default=0, help="streaming split-KV chunk (0 = auto)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -86,6 +86,7 @@ typedef struct {
                                   ("literal cascade") | 2 no node SEPARATE (all folded)        */
   int32_t split_tokens;        /* streaming split-KV chunk in tokens, 0 = auto (plan only)       */
   int32_t num_sms;             /* SM count the plan is sized for, 0 = 148 (B200)                */
+  int32_t dense_split;         /* split-KV factor of dense items, 0 = auto (plan only)            */
 } blend_build_args;
 
 typedef struct blend_tree blend_tree;   /* opaque, host-owned */

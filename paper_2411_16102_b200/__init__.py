@@ -43,7 +43,8 @@ class BuildArgs(C.Structure):
                 ("kv_dtype", C.c_int32), ("model_params", C.c_int64), ("hidden", C.c_int32),
                 ("layers", C.c_int32), ("page_size", C.c_int32), ("free_pages", C.c_void_p),
                 ("n_free_pages", C.c_int64), ("rows_min", C.c_int32), ("min_sep_len", C.c_int32),
-                ("force_class", C.c_int32), ("split_tokens", C.c_int32), ("num_sms", C.c_int32)]
+                ("force_class", C.c_int32), ("split_tokens", C.c_int32), ("num_sms", C.c_int32),
+                ("dense_split", C.c_int32)]
 
 
 class TreeView(C.Structure):
@@ -239,7 +240,7 @@ class Tree:
 def build(tokens, tok_off, q_len, prompt_len, out_len, *, num_q_heads, num_kv_heads, head_dim,
           kv_dtype="bf16", model_params=8_030_261_248, hidden=4096, layers=32, page_size=64,
           free_pages=None, global_id=None, rows_min=128, min_sep_len=128, force_class=0,
-          split_tokens=0, num_sms=148) -> Tree:
+          split_tokens=0, num_sms=148, dense_split=0) -> Tree:
     """blend_tree_build on host arrays (numpy-convertible)."""
     keep = []
     tok_off, p_off = _arr(tok_off, np.int64); keep.append(tok_off)
@@ -259,7 +260,7 @@ def build(tokens, tok_off, q_len, prompt_len, out_len, *, num_q_heads, num_kv_he
         fp, a.free_pages = _arr(free_pages, np.int32); keep.append(fp)
         a.n_free_pages = len(fp)
     a.rows_min, a.min_sep_len, a.force_class = rows_min, min_sep_len, force_class
-    a.split_tokens, a.num_sms = split_tokens, num_sms
+    a.split_tokens, a.num_sms, a.dense_split = split_tokens, num_sms, dense_split
     h = C.c_void_p()
     _check(lib().blend_tree_build(C.byref(a), C.byref(h)))
     return Tree(h.value)

@@ -13,6 +13,7 @@ extern "C" int blend_internal_plan_image(const blend_tree* t, const void** data,
 extern "C" int blend_internal_tree_dims(const blend_tree* t, int32_t* dims);
 extern "C" int64_t blend_internal_partial_rows(const blend_tree* t);
 extern "C" int64_t blend_internal_stream_entries(const blend_tree* t);
+extern "C" int64_t blend_internal_merge_unfused(const blend_tree* t);
 
 namespace blend {
 cudaError_t launch_generic(const AttnParams& p, cudaStream_t st);
@@ -52,6 +53,7 @@ extern "C" int blend_plan_upload(const blend_tree* tree, void* dev_buf, size_t b
   }
   plan->count[blend::SEC_COUNT] = blend_internal_partial_rows(tree);
   plan->count[blend::SEC_COUNT + 1] = blend_internal_stream_entries(tree);
+  plan->count[blend::SEC_COUNT + 2] = blend_internal_merge_unfused(tree);
   int32_t dims[5];
   blend_internal_tree_dims(tree, dims);
   plan->num_q_heads = dims[0];
@@ -127,7 +129,9 @@ extern "C" int blend_attention(const blend_attn_args* a, void* stream) {
   if (e != cudaSuccess) return cuda_fail(e);
 
   if (a->events[2]) cudaEventRecord((cudaEvent_t)a->events[2], st);
-  e = launch_merge(p, st);
+  AttnParams pm = p;
+  pm.n_merge = (int32_t)pl.count[SEC_COUNT + 2];   // fused lists are merged by the streaming pass
+  e = launch_merge(pm, st);
   if (e != cudaSuccess) return cuda_fail(e);
   if (a->events[3]) cudaEventRecord((cudaEvent_t)a->events[3], st);
   e = cudaPeekAtLastError();

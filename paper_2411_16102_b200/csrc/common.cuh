@@ -75,4 +75,40 @@ __device__ __forceinline__ int32_t row_target(const AttnParams& p, const Unit& u
   return p.partmap[u.pm_base + tl];
 }
 
+// Fused LSE merge (reading #17, ascending key start): this unit's own normalised
+// result (o_self[k] for elements e0 + k*stride, lse2_self) is combined with the
+// already-written partials of merge list m (entry -1 = self) and stored to out/lse.
+__device__ __forceinline__ void fused_merge_store(const AttnParams& p, int32_t tgt, int token, int head,
+                                                  const float* o_self, float lse2_self, int e0, int stride, int n,
+                                                  bool write_lse) {
+  const int m = PM_FUSED_BASE - tgt;
+  const int s0 = p.merge_off[m], s1 = p.merge_off[m + 1];
+  float M = -INFINITY;
+  for (int s = s0; s < s1; ++s) {
+    const int32_t row = p.merge_rows[s];
+    M = fmaxf(M, row < 0 ? lse2_self : p.ws_lse[(int64_t)row * p.hq + head]);
+  }
+  float acc[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) acc[k] = 0.f;
+  float tot = 0.f;
+  if (M != -INFINITY) {
+    for (int s = s0; s < s1; ++s) {
+      const int32_t row = p.merge_rows[s];
+      const float w = exp2f((row < 0 ? lse2_self : p.ws_lse[(int64_t)row * p.hq + head]) - M);
+      tot += w;
+      const float* src = p.ws_o + ((int64_t)row * p.hq + head) * p.d;
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        if (k < n) acc[k] = fmaf(w, row < 0 ? o_self[k] : src[e0 + k * stride], acc[k]);
+    }
+  }
+  const float inv = tot > 0.f ? 1.f / tot : 0.f;
+  const int64_t ob = ((int64_t)token * p.hq + head) * p.d;
+#pragma unroll
+  for (int k = 0; k < 16; ++k)
+    if (k < n) st_elem(p.out, ob + e0 + k * stride, acc[k] * inv, p.kv_f32);
+  if (write_lse) p.lse[(int64_t)token * p.hq + head] = M != -INFINITY ? (M + log2f(tot)) * kLn2 : -INFINITY;
+}
+
 }  // namespace blend

@@ -101,6 +101,7 @@ struct blend_tree {
   size_t workspace_bytes = 0;
   int64_t n_partial_rows = 0;
   int64_t stream_entries = 0;   // sum over stream units of their entry counts (launch heuristic)
+  int32_t n_merge_unfused = 0;  // merge lists [0, n) are merged by the merge kernel
 };
 
 namespace {
@@ -123,7 +124,7 @@ int validate(const blend_build_args* a) {
     return fail(BLEND_EINVAL, "page_size must be a power of two in [16,128]");
   if (a->kv_dtype != BLEND_BF16 && a->kv_dtype != BLEND_F32) return fail(BLEND_EINVAL, "kv_dtype");
   if (a->rows_min < 0 || a->min_sep_len < -1 || a->force_class < 0 || a->force_class > 2 ||
-      a->split_tokens < 0 || a->num_sms < 0)
+      a->split_tokens < 0 || a->num_sms < 0 || a->dense_split < 0)
     return fail(BLEND_EINVAL, "rows_min/min_sep_len/force_class/split_tokens/num_sms");
   if (a->n_req < 1) return fail(BLEND_EINVAL, "n_req must be >= 1");
   if (!a->tok_off || !a->tokens || !a->q_len || !a->prompt_len || !a->out_len)
@@ -530,7 +531,8 @@ int build_plan(blend_tree* t) {
   }
   // dense split-KV: fill (at most) one wave of persistent CTAs without exceeding it
   int64_t dsplit = 1;
-  if (base_d > 0 && base_d < num_sms) dsplit = num_sms / base_d;
+  if (a.dense_split > 0) dsplit = a.dense_split;
+  else if (base_d > 0 && base_d < num_sms) dsplit = num_sms / base_d;
 
   std::vector<std::vector<int32_t>> split_b(items.size());   // entry boundaries per item
   for (size_t ii = 0; ii < items.size(); ++ii) {
@@ -578,6 +580,7 @@ int build_plan(blend_tree* t) {
   std::vector<int32_t> nsrc(T, 0);
   struct Src {
     int32_t tok, key_start, pm;
+    bool dense;
   };
   std::vector<Src> srcs;
   for (size_t ii = 0; ii < items.size(); ++ii) {
@@ -588,7 +591,7 @@ int build_plan(blend_tree* t) {
         int32_t tk = it.toks[i];
         if (ks <= tok_pos[tk]) {
           nsrc[tk] += 1;
-          srcs.push_back({tk, ks, pm_base[ii][s] + (int32_t)i});
+          srcs.push_back({tk, ks, pm_base[ii][s] + (int32_t)i, it.dense});
         }
       }
     }
@@ -598,22 +601,45 @@ int build_plan(blend_tree* t) {
   std::stable_sort(srcs.begin(), srcs.end(), [](const Src& x, const Src& y) {
     return x.tok != y.tok ? x.tok < y.tok : x.key_start < y.key_start;
   });
-  std::vector<int32_t> merge_tok, merge_off{0}, merge_rows;
-  int64_t prow = 0;
+  // Merge lists, ascending key start.  A token whose only streaming source is a
+  // single (item, split) and whose other sources are all dense-pass partials is
+  // merged by that streaming unit itself ("fused"): the dense pass has completed
+  // on the stream before the streaming pass starts.  Its list holds -1 for the
+  // streaming unit's own in-register result; fused tokens follow the unfused ones.
+  struct Group {
+    size_t i, j;
+    bool fused;
+  };
+  std::vector<Group> groups;
   for (size_t i = 0; i < srcs.size();) {
     size_t j = i;
-    while (j < srcs.size() && srcs[j].tok == srcs[i].tok) ++j;
+    int n_stream = 0;
+    while (j < srcs.size() && srcs[j].tok == srcs[i].tok) n_stream += srcs[j++].dense ? 0 : 1;
     if (j - i == 1) partmap[srcs[i].pm] = blend::PM_DIRECT;
-    else {
-      merge_tok.push_back(srcs[i].tok);
-      for (size_t k = i; k < j; ++k) {
-        partmap[srcs[k].pm] = (int32_t)prow;
-        merge_rows.push_back((int32_t)prow++);
-      }
-      merge_off.push_back((int32_t)merge_rows.size());
-    }
+    else groups.push_back({i, j, n_stream == 1});
     i = j;
   }
+  std::vector<int32_t> merge_tok, merge_off{0}, merge_rows;
+  int64_t prow = 0;
+  int32_t n_unfused = 0;
+  for (int pass = 0; pass < 2; ++pass)
+    for (const Group& gr : groups) {
+      if (gr.fused != (pass == 1)) continue;
+      const int32_t m = (int32_t)merge_tok.size();
+      merge_tok.push_back(srcs[gr.i].tok);
+      for (size_t k = gr.i; k < gr.j; ++k) {
+        if (gr.fused && !srcs[k].dense) {
+          partmap[srcs[k].pm] = blend::PM_FUSED_BASE - m;
+          merge_rows.push_back(-1);
+        } else {
+          partmap[srcs[k].pm] = (int32_t)prow;
+          merge_rows.push_back((int32_t)prow++);
+        }
+      }
+      merge_off.push_back((int32_t)merge_rows.size());
+      if (pass == 0) ++n_unfused;
+    }
+  t->n_merge_unfused = n_unfused;
   if (prow > INT32_MAX / 2) return fail(BLEND_EINVAL, "too many partial rows");
 
   // ---- entries and units
@@ -924,6 +950,7 @@ int blend_internal_fail(int status, const char* msg) { return fail(status, "%s",
 
 int64_t blend_internal_partial_rows(const blend_tree* t) { return t ? t->n_partial_rows : 0; }
 int64_t blend_internal_stream_entries(const blend_tree* t) { return t ? t->stream_entries : 0; }
+int64_t blend_internal_merge_unfused(const blend_tree* t) { return t ? t->n_merge_unfused : 0; }
 
 int blend_internal_tree_dims(const blend_tree* t, int32_t* dims) {
   if (!t) return fail(BLEND_EINVAL, "tree is NULL");

@@ -16,12 +16,13 @@ enum PlanSection {
   SEC_PARTMAP,         // int32[]    per (item, split) x item token: partial row | DIRECT | SKIP
   SEC_MERGE_TOK,       // int32[M]   tokens with >= 2 sources
   SEC_MERGE_OFF,       // int32[M+1]
-  SEC_MERGE_ROWS,      // int32[]    partial rows, ascending key-range start
+  SEC_MERGE_ROWS,      // int32[]    partial rows, ascending key-range start (-1 = the fusing unit)
   SEC_COUNT
 };
 
 constexpr int32_t PM_DIRECT = -1;   // the only source of this token: write out/lse directly
 constexpr int32_t PM_SKIP = -2;     // this (item, split) has no key at or before the token
+constexpr int32_t PM_FUSED_BASE = -3;  // <= -3: streaming unit merges list m = PM_FUSED_BASE - value itself
 
 // One KV page entry: <= 64 consecutive slots of one physical page.
 struct KvEntry {

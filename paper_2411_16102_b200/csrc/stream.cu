@@ -5,15 +5,19 @@
 // Per SURVEY §8(a-8) / PAPER §2.3 P:92-96 (decode "loads all p+i tokens"; with
 // cascade the private part only, §7.2): the pass reads each K/V page-head
 // block once per unit, so it is bound by HBM bandwidth.  Design (B200):
-//   * persistent CTAs (one per SM), static unit striding (units sorted longest first);
+//   * persistent CTAs (1 per SM for long units, 2 per SM for short decode units),
+//     static unit striding (units sorted longest first);
 //   * a TMA producer warp streams 64-slot K/V page entries with
-//     cp.async.bulk.tensor (128B swizzle) into an mbarrier ring of stages;
+//     cp.async.bulk.tensor (128B swizzle) into an mbarrier ring of stages, loading
+//     only the 16-row groups that hold valid slots of a partial page;
 //   * 4 consumer warps split each stage's 64 keys (16 each): S = Q K^T and
 //     O += P V on the legacy tensor pipe (mma.sync m16n8k16 bf16, fp32 accumulate;
 //     at intensity g FLOP/B the FP32 FMA pipe would not keep up for g = 8),
 //     warp-shuffle online softmax in the log2 domain;
 //   * the 4 warp states are LSE-combined in shared memory at the unit end and
-//     written as the final bf16 row (single-source token) or an fp32 partial.
+//     written as the final bf16 row (single-source token), an fp32 partial, or —
+//     when the token's other sources are dense-pass partials — merged with those
+//     in place (fused LSE merge, no separate merge launch for the token).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <math.h>
@@ -49,7 +53,8 @@ __host__ __device__ inline StreamSmem stream_smem_layout(int D, int nstage) {
 
 template <int D>
 __global__ void __launch_bounds__(ST_THREADS, 2)
-    stream_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv, AttnParams p,
+    stream_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
+                  const __grid_constant__ CUtensorMap tmk16, const __grid_constant__ CUtensorMap tmv16, AttnParams p,
                   int nstage, int box_rows) {
   constexpr int CH = D / 64;       // 128-B chunks per row
   constexpr int NT = D / 8;        // output n-tiles
@@ -74,7 +79,8 @@ __global__ void __launch_bounds__(ST_THREADS, 2)
     if (lane == 0) {
       ptx::tma_prefetch_desc(&tmk);
       ptx::tma_prefetch_desc(&tmv);
-      const uint32_t bytes = 2u * CH * box_rows * 128u;
+      ptx::tma_prefetch_desc(&tmk16);
+      ptx::tma_prefetch_desc(&tmv16);
       uint32_t it = 0;
       for (int ui = blockIdx.x; ui < p.n_units; ui += gridDim.x) {
         const Unit u = p.units[ui];
@@ -84,11 +90,22 @@ __global__ void __launch_bounds__(ST_THREADS, 2)
           const KvEntry en = p.entries[e];
           const int32_t y = (en.page * p.hkv + u.kvh) * p.ps + en.row_off;
           uint8_t* st = smem + L.stage0 + s * L.stage_stride;
-          ptx::mbar_arrive_expect_tx(&full[s], bytes);
+          // load only the 16-row groups that hold valid slots (a node's last page is partial)
+          const int rows = (en.count + 15) & ~15;
+          ptx::mbar_arrive_expect_tx(&full[s], 2u * CH * rows * 128u);
+          if (rows == box_rows) {
 #pragma unroll
-          for (int c = 0; c < CH; ++c) {
-            ptx::tma_load_2d(st + c * ST_CHUNK_BYTES, &tmk, &full[s], c * 64, y);
-            ptx::tma_load_2d(st + (CH + c) * ST_CHUNK_BYTES, &tmv, &full[s], c * 64, y);
+            for (int c = 0; c < CH; ++c) {
+              ptx::tma_load_2d(st + c * ST_CHUNK_BYTES, &tmk, &full[s], c * 64, y);
+              ptx::tma_load_2d(st + (CH + c) * ST_CHUNK_BYTES, &tmv, &full[s], c * 64, y);
+            }
+          } else {
+            for (int r0 = 0; r0 < rows; r0 += 16)
+#pragma unroll
+              for (int c = 0; c < CH; ++c) {
+                ptx::tma_load_2d(st + c * ST_CHUNK_BYTES + r0 * 128, &tmk16, &full[s], c * 64, y + r0);
+                ptx::tma_load_2d(st + (CH + c) * ST_CHUNK_BYTES + r0 * 128, &tmv16, &full[s], c * 64, y + r0);
+              }
           }
         }
       }
@@ -248,11 +265,12 @@ __global__ void __launch_bounds__(ST_THREADS, 2)
       mw[16 * D + 16 + g8] = l0;
       mw[16 * D + 16 + g8 + 8] = l1;
     }
+    const bool w0 = g8 < u.n_rows, w1 = g8 + 8 < u.n_rows;   // padding rows are never read
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
       const int d0 = 8 * j + 2 * c4;
-      *reinterpret_cast<float2*>(mw + g8 * D + d0) = make_float2(o[j][0], o[j][1]);
-      *reinterpret_cast<float2*>(mw + (g8 + 8) * D + d0) = make_float2(o[j][2], o[j][3]);
+      if (w0) *reinterpret_cast<float2*>(mw + g8 * D + d0) = make_float2(o[j][0], o[j][1]);
+      if (w1) *reinterpret_cast<float2*>(mw + (g8 + 8) * D + d0) = make_float2(o[j][2], o[j][3]);
     }
     ptx::named_bar_sync(1, 128);
     {
@@ -282,7 +300,9 @@ __global__ void __launch_bounds__(ST_THREADS, 2)
           for (int w = 0; w < ST_CWARPS; ++w) a += coef[w] * mrg[w * (16 * D + 32) + r * D + dsl + k];
           ov[k] = a * inv;
         }
-        if (tgt == PM_DIRECT) {
+        if (tgt <= PM_FUSED_BASE) {
+          fused_merge_store(p, tgt, token, head, ov, lse2, dsl, 1, D / 8, (tid & 7) == 0);
+        } else if (tgt == PM_DIRECT) {
           __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.out) + ((int64_t)token * p.hq + head) * D + dsl;
 #pragma unroll
           for (int k = 0; k < D / 8; k += 8) {
@@ -351,11 +371,12 @@ int num_sms_cached() {
 template <int D>
 static cudaError_t launch_stream_d(const AttnParams& p, int64_t n_cache_pages, cudaStream_t st) {
   const int box_rows = p.ps < ST_KEYS ? p.ps : ST_KEYS;
-  CUtensorMap tk, tv;
+  CUtensorMap tk, tv, tk16, tv16;
   const int64_t rows = n_cache_pages * p.hkv * p.ps;
   cudaError_t e = make_cache_tmap(&tk, p.k_cache, rows, D, box_rows);
-  if (e != cudaSuccess) return e;
-  e = make_cache_tmap(&tv, p.v_cache, rows, D, box_rows);
+  if (e == cudaSuccess) e = make_cache_tmap(&tv, p.v_cache, rows, D, box_rows);
+  if (e == cudaSuccess) e = make_cache_tmap(&tk16, p.k_cache, rows, D, 16);
+  if (e == cudaSuccess) e = make_cache_tmap(&tv16, p.v_cache, rows, D, 16);
   if (e != cudaSuccess) return e;
   // Short units (decode over a ~100-token private suffix): 2 CTAs per SM with a 2-stage
   // ring each, so one CTA's per-unit prologue/epilogue overlaps the other's streaming.
@@ -370,7 +391,7 @@ static cudaError_t launch_stream_d(const AttnParams& p, int64_t n_cache_pages, c
   if (e != cudaSuccess) return e;
   const int slots = ctas_per_sm * num_sms_cached();
   const int grid = p.n_units < slots ? p.n_units : slots;
-  stream_kernel<D><<<grid, ST_THREADS, smem, st>>>(tk, tv, p, nstage, box_rows);
+  stream_kernel<D><<<grid, ST_THREADS, smem, st>>>(tk, tv, tk16, tv16, p, nstage, box_rows);
   return cudaPeekAtLastError();
 }
 

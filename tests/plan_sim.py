@@ -58,7 +58,9 @@ def simulate(w, tree):
     out = np.full((T, Hq, D), np.nan)
     lse = np.full((T, Hq), np.nan)
     written = np.zeros((T, Hq), dtype=np.int64)
-    for units in (P["dunits"], P["sunits"]):
+    fused = {}
+    dense_rows = set()
+    for kind, units in (("dense", P["dunits"]), ("stream", P["sunits"])):
         for u in units:
             item, kvh, rb, nr, eb, ee, pmb, tb = (int(x) for x in u)
             kpos, K, Vv = [], [], []
@@ -81,17 +83,35 @@ def simulate(w, tree):
                 tgt = int(P["partmap"][pmb + tl])
                 if tgt == -2:
                     continue
+                if tgt <= -3:                       # fused: this unit merges list m itself
+                    fused[(tok, head)] = (o[0, 0], l[0, 0])
+                    continue
                 if tgt == -1:
                     out[tok, head], lse[tok, head] = o[0, 0], l[0, 0]
                     written[tok, head] += 1
                 else:
                     assert np.isnan(part_l[tgt, head]), "partial row written twice"
                     part_o[tgt, head], part_l[tgt, head] = o[0, 0], l[0, 0]
+                    if kind == "dense":
+                        dense_rows.add(tgt)
     mo = P["merge_off"]
     for m, tok in enumerate(P["merge_tok"]):
         rows = P["merge_rows"][mo[m]:mo[m + 1]]
-        assert not np.isnan(part_l[rows]).any(), "merge reads an unwritten partial"
-        O, L = A.lse_merge([(part_o[r][None], part_l[r][None]) for r in rows])
-        out[tok], lse[tok] = O[0], L[0]
+        real = [r for r in rows if r >= 0]
+        assert not np.isnan(part_l[real]).any(), "merge reads an unwritten partial"
+        assert sum(1 for r in rows if r < 0) <= 1
+        if any(r < 0 for r in rows):          # fused by a streaming unit: only dense-pass partials
+            assert all(r in dense_rows for r in real), "fused list reads a streaming partial"
+        for h in range(Hq):
+            parts = []
+            for r in rows:
+                if r >= 0:
+                    parts.append((part_o[r, h][None, None], part_l[r, h][None, None]))
+                else:
+                    fo, fl = fused.pop((int(tok), h))
+                    parts.append((fo[None, None], np.array([[fl]])))
+            O, L = A.lse_merge(parts)
+            out[tok, h], lse[tok, h] = O[0, 0], L[0, 0]
         written[tok] += 1
+    assert not fused, "fused results never merged"
     return out, lse, written, P
