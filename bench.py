@@ -251,10 +251,17 @@ def run_ours(args):
     torch.cuda.synchronize()
 
     K = args.steps
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
-    for row in ev:            # torch creates CUDA events lazily: materialise the handles
-        for e in row:
-            e.record(stream)
+    def mk_events(n, m):
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(m)] for _ in range(n)]
+        for row in evs:       # torch creates CUDA events lazily: materialise the handles
+            for e in row:
+                e.record(stream)
+        return evs
+
+    # ---- timed region: K whole steps (dense || streaming via PDL, then merge), events at the ends
+    ev = mk_events(K, 2)
+    # ---- per-pass breakdown: K serialised steps with events between the passes (roofline)
+    evp = mk_events(K, 4)
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
@@ -265,23 +272,29 @@ def run_ours(args):
     for k in range(K):
         if do_flush:
             B.l2_flush(flush)
-        db.run(path=path, events=ev[k])
+        db.run(path=path, events=[ev[k][0], None, None, ev[k][1]])
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
-    t_step = [ev[k][0].elapsed_time(ev[k][3]) for k in range(K)]
-    t_dense = [ev[k][0].elapsed_time(ev[k][1]) for k in range(K)]
-    t_stream = [ev[k][1].elapsed_time(ev[k][2]) for k in range(K)]
-    t_merge = [ev[k][2].elapsed_time(ev[k][3]) for k in range(K)]
+    for k in range(K):
+        if do_flush:
+            B.l2_flush(flush)
+        db.run(path=path, events=evp[k], flags=B.SERIALIZE)
+    torch.cuda.synchronize()
+    t_step = [ev[k][0].elapsed_time(ev[k][1]) for k in range(K)]
+    t_ser = [evp[k][0].elapsed_time(evp[k][3]) for k in range(K)]
+    t_dense = [evp[k][0].elapsed_time(evp[k][1]) for k in range(K)]
+    t_stream = [evp[k][1].elapsed_time(evp[k][2]) for k in range(K)]
+    t_merge = [evp[k][2].elapsed_time(evp[k][3]) for k in range(K)]
     ms = float(np.mean(t_step))
-    loc = torch.tensor([ms, float(np.mean(t_dense)), float(np.mean(t_stream)), float(np.mean(t_merge))],
-                       dtype=torch.float64, device="cuda")
+    loc = torch.tensor([ms, float(np.mean(t_dense)), float(np.mean(t_stream)), float(np.mean(t_merge)),
+                        float(np.mean(t_ser))], dtype=torch.float64, device="cuda")
     tok = torch.tensor([float(w.sum_q)], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(loc, op=dist.ReduceOp.MAX)
         dist.all_reduce(tok, op=dist.ReduceOp.SUM)
-    ms, md, mst, mm = loc.tolist()
+    ms, md, mst, mm, mser = loc.tolist()
     total_tok = tok.item()
     value = total_tok / (ms * 1e-3)
 
@@ -327,7 +340,7 @@ def run_ours(args):
         gather_ms = g0.elapsed_time(g1)
 
     launches_per_step = int(info["n_dense_units"] > 0) + int(info["n_stream_units"] > 0) + \
-        int(info["n_merge_tokens"] > 0)
+        int(info["n_merge_tokens"] > 0)   # merge launch count assumes unfused lists (bench default)
 
     # ---- roofline of the dominant kernel (per launch, CUDA events on the launching stream)
     peaks = load_peaks()
@@ -370,7 +383,9 @@ def run_ours(args):
             "gpu_launches": launches_per_step * K,
             "roofline": roof,
             "cpu_baseline": cpu,
-            "passes_ms": {"dense": md, "stream": mst, "merge": mm},
+            "passes_ms": {"dense": md, "stream": mst, "merge": mm, "serialized_step": mser,
+                          "note": "per-pass times from K extra steps run with BLEND_SERIALIZE; the timed "
+                                  "steps overlap the dense and streaming passes (PDL)"},
             "work": {"F_alg": F, "B_alg": Bytes, "kv_bytes": KVb, **pw,
                      "whole_step_roofline_frac_measured": max(F / (load_peaks()["bf16_tflops"] * 1e12),
                                                               Bytes / (load_peaks()["hbm_gbs"] * 1e9)) / (ms * 1e-3)},

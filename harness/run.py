@@ -16,14 +16,14 @@ from synth import values as V
 
 
 def build_tree(w, rows_min=128, min_sep_len=128, force_class=0, split_tokens=0, num_sms=148,
-               free_pages=None, dense_split=0):
+               free_pages=None, dense_split=0, fuse_merge=0):
     fp = w.free_pages if free_pages is None else free_pages
     return B.build(w.tokens, w.tok_off, w.q_len, w.prompt_len, w.out_len,
                    num_q_heads=w.num_q_heads, num_kv_heads=w.num_kv_heads, head_dim=w.head_dim,
                    kv_dtype=w.kv_dtype, model_params=w.model_params, hidden=w.hidden, layers=w.layers,
                    page_size=w.page_size, free_pages=fp, global_id=w.global_id, rows_min=rows_min,
                    min_sep_len=min_sep_len, force_class=force_class, split_tokens=split_tokens,
-                   num_sms=num_sms, dense_split=dense_split)
+                   num_sms=num_sms, dense_split=dense_split, fuse_merge=fuse_merge)
 
 
 def page_slot_hashes(w, view):
@@ -75,9 +75,10 @@ class DeviceBatch:
     build_s: float
     info: dict
 
-    def run(self, path=B.PATH_AUTO, stream=None, events=None):
+    def run(self, path=B.PATH_AUTO, stream=None, events=None, flags=0):
         B.attention(self.q, self.k_cache, self.v_cache, self.plan, self.out, self.lse, self.ws,
-                    n_cache_pages=self.n_cache_pages, path=path, stream=stream, events=events)
+                    n_cache_pages=self.n_cache_pages, path=path, stream=stream, events=events,
+                    flags=flags)
 
 
 def device_batch(w, device="cuda", tree_kw=None, n_cache_pages=None, fill=True) -> DeviceBatch:

@@ -87,6 +87,8 @@ typedef struct {
   int32_t split_tokens;        /* streaming split-KV chunk in tokens, 0 = auto (plan only)       */
   int32_t num_sms;             /* SM count the plan is sized for, 0 = 148 (B200)                */
   int32_t dense_split;         /* split-KV factor of dense items, 0 = auto (plan only)            */
+  int32_t fuse_merge;          /* 1: a streaming unit whose token's other sources are dense
+                                  partials merges them itself (no merge launch); 0 = off       */
 } blend_build_args;
 
 typedef struct blend_tree blend_tree;   /* opaque, host-owned */
@@ -185,6 +187,7 @@ int blend_plan_upload(const blend_tree* tree, void* dev_buf, size_t bytes, void*
                       blend_plan* plan);
 
 enum { BLEND_PATH_AUTO = 0, BLEND_PATH_GENERIC = 1, BLEND_PATH_NO_TCGEN05 = 2 };
+enum { BLEND_SERIALIZE = 1 };
 
 typedef struct {
   const void* q;             /* device [sum q, Hq, D] (kv dtype), rows in caller request order:
@@ -200,10 +203,15 @@ typedef struct {
   const blend_plan* plan;    /* from blend_plan_upload (its buffer must be resident)         */
   int32_t path;              /* BLEND_PATH_*: AUTO = tcgen05 dense + streaming (+ generic for
                                 fp32); GENERIC = every unit on the fp32-FMA item executor;
-                                NO_TCGEN05 = dense units on the streaming executor          */
-  int32_t reserved;
+                                NO_TCGEN05 = dense units on the generic executor            */
+  int32_t flags;             /* BLEND_SERIALIZE: run the passes back to back.  Default: the
+                                streaming pass is launched with programmatic dependent launch
+                                and overlaps the dense pass on free SMs (the two passes are
+                                independent; the streaming grid completes only after the
+                                dense grid, so the merge sees both)                        */
   void* events[4];           /* optional cudaEvent_t recorded before dense, before stream,
-                                before merge, after merge (NULL entries skipped)           */
+                                before merge, after merge (NULL entries skipped); non-NULL
+                                events[1] or events[2] imply BLEND_SERIALIZE                 */
 } blend_attn_args;
 
 /* Enqueue the blended-batch attention on stream.  Every slot of every page the

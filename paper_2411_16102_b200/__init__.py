@@ -26,6 +26,7 @@ LIB_PATH = os.path.join(_HERE, "libblend.so")
 OK, EINVAL, EMALFORMED, ENOSPC, ECUDA, ENOMEM, EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
 BF16, F32 = 0, 1
 PATH_AUTO, PATH_GENERIC, PATH_NO_TCGEN05 = 0, 1, 2
+SERIALIZE = 1
 _DTYPES = {"bf16": BF16, "f32": F32}
 
 
@@ -44,7 +45,7 @@ class BuildArgs(C.Structure):
                 ("layers", C.c_int32), ("page_size", C.c_int32), ("free_pages", C.c_void_p),
                 ("n_free_pages", C.c_int64), ("rows_min", C.c_int32), ("min_sep_len", C.c_int32),
                 ("force_class", C.c_int32), ("split_tokens", C.c_int32), ("num_sms", C.c_int32),
-                ("dense_split", C.c_int32)]
+                ("dense_split", C.c_int32), ("fuse_merge", C.c_int32)]
 
 
 class TreeView(C.Structure):
@@ -72,7 +73,7 @@ class AttnArgs(C.Structure):
     _fields_ = [("q", C.c_void_p), ("k_cache", C.c_void_p), ("v_cache", C.c_void_p),
                 ("n_cache_pages", C.c_int64), ("out", C.c_void_p), ("lse", C.c_void_p),
                 ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
-                ("plan", C.POINTER(Plan)), ("path", C.c_int32), ("reserved", C.c_int32),
+                ("plan", C.POINTER(Plan)), ("path", C.c_int32), ("flags", C.c_int32),
                 ("events", C.c_void_p * 4)]
 
 
@@ -240,7 +241,7 @@ class Tree:
 def build(tokens, tok_off, q_len, prompt_len, out_len, *, num_q_heads, num_kv_heads, head_dim,
           kv_dtype="bf16", model_params=8_030_261_248, hidden=4096, layers=32, page_size=64,
           free_pages=None, global_id=None, rows_min=128, min_sep_len=128, force_class=0,
-          split_tokens=0, num_sms=148, dense_split=0) -> Tree:
+          split_tokens=0, num_sms=148, dense_split=0, fuse_merge=0) -> Tree:
     """blend_tree_build on host arrays (numpy-convertible)."""
     keep = []
     tok_off, p_off = _arr(tok_off, np.int64); keep.append(tok_off)
@@ -261,13 +262,14 @@ def build(tokens, tok_off, q_len, prompt_len, out_len, *, num_q_heads, num_kv_he
         a.n_free_pages = len(fp)
     a.rows_min, a.min_sep_len, a.force_class = rows_min, min_sep_len, force_class
     a.split_tokens, a.num_sms, a.dense_split = split_tokens, num_sms, dense_split
+    a.fuse_merge = fuse_merge
     h = C.c_void_p()
     _check(lib().blend_tree_build(C.byref(a), C.byref(h)))
     return Tree(h.value)
 
 
 def attention(q, k_cache, v_cache, plan: Plan, out, lse, workspace, *, n_cache_pages: int,
-              stream=None, path: int = PATH_AUTO, events=None) -> None:
+              stream=None, path: int = PATH_AUTO, events=None, flags: int = 0) -> None:
     """blend_attention: enqueue on `stream` (default: torch's current stream)."""
     a = AttnArgs()
     a.q, a.k_cache, a.v_cache = q.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr()
@@ -278,6 +280,7 @@ def attention(q, k_cache, v_cache, plan: Plan, out, lse, workspace, *, n_cache_p
         a.workspace_bytes = workspace.numel() * workspace.element_size()
     a.plan = C.pointer(plan)
     a.path = path
+    a.flags = flags
     if events:
         for i, ev in enumerate(events[:4]):
             a.events[i] = None if ev is None else ev.cuda_event

@@ -17,8 +17,8 @@ extern "C" int64_t blend_internal_merge_unfused(const blend_tree* t);
 
 namespace blend {
 cudaError_t launch_generic(const AttnParams& p, cudaStream_t st);
-cudaError_t launch_merge(const AttnParams& p, cudaStream_t st);
-cudaError_t launch_stream(const AttnParams& p, int64_t n_cache_pages, cudaStream_t st);
+cudaError_t launch_merge(const AttnParams& p, cudaStream_t st, bool pdl);
+cudaError_t launch_stream(const AttnParams& p, int64_t n_cache_pages, cudaStream_t st, bool overlap);
 cudaError_t launch_dense(const AttnParams& p, int64_t n_cache_pages, cudaStream_t st);
 }  // namespace blend
 
@@ -72,6 +72,7 @@ extern "C" int blend_attention(const blend_attn_args* a, void* stream) {
   const blend_plan& pl = *a->plan;
   if (!pl.dev) return blend_internal_fail(BLEND_EINVAL, "attention: plan not uploaded");
   if (a->path < 0 || a->path > 2) return blend_internal_fail(BLEND_EINVAL, "attention: bad path");
+  if (a->flags & ~BLEND_SERIALIZE) return blend_internal_fail(BLEND_EINVAL, "attention: bad flags");
   static int arch_ok = -1;
   if (arch_ok < 0) arch_ok = check_arch() == BLEND_OK ? 1 : 0;
   if (!arch_ok) return blend_internal_fail(BLEND_EUNSUPPORTED, "libblend is built for sm_100a (B200)");
@@ -109,6 +110,11 @@ extern "C" int blend_attention(const blend_attn_args* a, void* stream) {
   p.scale_log2 = kLog2e / sqrtf((float)D);
   cudaStream_t st = (cudaStream_t)stream;
   const bool generic = a->path == BLEND_PATH_GENERIC || p.kv_f32;
+  const int64_t n_merge_all = pl.count[SEC_MERGE_TOK], n_merge_unfused = pl.count[SEC_COUNT + 2];
+  // PDL overlap of the independent dense and streaming passes, unless serialisation is
+  // requested, per-pass events are wanted, or fused merges read dense partials
+  const bool overlap = !generic && !(a->flags & BLEND_SERIALIZE) && !a->events[1] && !a->events[2] &&
+                       n_merge_all == n_merge_unfused;
   cudaError_t e;
 
   if (a->events[0]) cudaEventRecord((cudaEvent_t)a->events[0], st);
@@ -125,13 +131,13 @@ extern "C" int blend_attention(const blend_attn_args* a, void* stream) {
   ps_.n_units = (int32_t)pl.count[SEC_STREAM_UNITS];
   ps_.avg_entries = ps_.n_units > 0 ? (int32_t)(pl.count[SEC_COUNT + 1] / ps_.n_units) : 0;
   if (generic) e = launch_generic(ps_, st);
-  else e = launch_stream(ps_, a->n_cache_pages, st);
+  else e = launch_stream(ps_, a->n_cache_pages, st, overlap);
   if (e != cudaSuccess) return cuda_fail(e);
 
   if (a->events[2]) cudaEventRecord((cudaEvent_t)a->events[2], st);
   AttnParams pm = p;
   pm.n_merge = (int32_t)pl.count[SEC_COUNT + 2];   // fused lists are merged by the streaming pass
-  e = launch_merge(pm, st);
+  e = launch_merge(pm, st, overlap);
   if (e != cudaSuccess) return cuda_fail(e);
   if (a->events[3]) cudaEventRecord((cudaEvent_t)a->events[3], st);
   e = cudaPeekAtLastError();

@@ -76,6 +76,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  ptx::pdl_launch_dependents();   // the streaming pass may start on SMs this grid leaves free
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       ptx::mbar_init(&kv_full[s], 1);
@@ -95,7 +96,10 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-
+  // register budget: warpgroup 0 (producer, MMA, allocator) needs few; the two softmax
+  // warpgroups keep a 128-score row in registers (48*128 + 232*256 = 64K registers)
+  if (warp < 4) {
+  ptx::setmaxnreg_dec<48>();
   if (warp == 0) {
     // ===================== TMA producer =====================
     if (lane == 0) {
@@ -193,7 +197,9 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         ++gu;
       }
     }
-  } else if (warp >= 4) {
+  }
+  } else {
+    ptx::setmaxnreg_inc<232>();
     // ===================== softmax / epilogue (tile t) =====================
     const int t = (warp - 4) >> 2;                    // 0 = tile A, 1 = tile B
     const int r = threadIdx.x - 128 - 128 * t;        // row within the tile = TMEM lane
@@ -249,18 +255,21 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         }
         ptx::mbar_wait(&s_full[t], sb & 1);
         ptx::tc_fence_after();
-        // pass 1: row max over the 128 scores (32-column chunks keep registers low)
+        // the whole 128-score row in registers (softmax warps run with 232 registers)
+        float sv[DN_KB];
+#pragma unroll
+        for (int c = 0; c < DN_KB / 32; ++c)
+          ptx::tmem_ld32(tmem + lane_base + col_s + c * 32, reinterpret_cast<uint32_t*>(sv + c * 32));
+        ptx::tmem_wait_ld();
         float mx = -INFINITY;
+        if (full_vis) {
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          float sv[32];
-          ptx::tmem_ld32(tmem + lane_base + col_s + h * 32, reinterpret_cast<uint32_t*>(sv));
-          ptx::tmem_wait_ld();
+          for (int k = 0; k < DN_KB; ++k) mx = fmaxf(mx, sv[k]);
+        } else {
 #pragma unroll
-          for (int k = 0; k < 32; ++k) {
-            const int key = h * 32 + k;
-            const bool ok = full_vis || (key % BOX) < vis[key / BOX];
-            mx = fmaxf(mx, ok ? sv[k] : -INFINITY);
+          for (int k = 0; k < DN_KB; ++k) {
+            sv[k] = (k % BOX) < vis[k / BOX] ? sv[k] : -INFINITY;
+            mx = fmaxf(mx, sv[k]);
           }
         }
         const float mx2 = mx * p.scale_log2;
@@ -284,25 +293,22 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         }
         const float m_use = m_ref == -INFINITY ? 0.f : m_ref;
         float lsum = 0.f;
-        // pass 2: P = exp2(s*scale - m) -> bf16 pairs -> TMEM columns [0, 64) (aliasing
-        // the already-consumed first half of S)
+        // P = exp2(s*scale - m): 3 of every 4 on the MUFU pipe, 1 of 4 as a polynomial on
+        // the FMA pipe (the two pipes run concurrently); bf16 pairs -> TMEM columns [0, 64)
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          float sv[32];
-          ptx::tmem_ld32(tmem + lane_base + col_s + h * 32, reinterpret_cast<uint32_t*>(sv));
-          ptx::tmem_wait_ld();
+        for (int c = 0; c < DN_KB / 32; ++c) {
           uint32_t pk[16];
 #pragma unroll
           for (int k = 0; k < 16; ++k) {
-            const int key = h * 32 + 2 * k;
-            const bool ok0 = full_vis || (key % BOX) < vis[key / BOX];
-            const bool ok1 = full_vis || ((key + 1) % BOX) < vis[(key + 1) / BOX];
-            const float p0 = ok0 ? ptx::ex2(fmaf(sv[2 * k], p.scale_log2, -m_use)) : 0.f;
-            const float p1 = ok1 ? ptx::ex2(fmaf(sv[2 * k + 1], p.scale_log2, -m_use)) : 0.f;
+            const int key = c * 32 + 2 * k;
+            const float x0 = fmaf(sv[key], p.scale_log2, -m_use);
+            const float x1 = fmaf(sv[key + 1], p.scale_log2, -m_use);
+            const float p0 = ptx::ex2(x0);
+            const float p1 = (k & 1) ? ptx::exp2_poly(x1) : ptx::ex2(x1);
             lsum += p0 + p1;
             pk[k] = ptx::pack_bf16(p0, p1);
           }
-          ptx::tmem_st16(tmem + lane_base + col_s + h * 16, pk);   // keys 32h.. -> columns 16h..
+          ptx::tmem_st16(tmem + lane_base + col_s + c * 16, pk);   // keys 32c.. -> columns 16c..
         }
         l += lsum;
         ptx::tmem_wait_st();
@@ -357,6 +363,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
 }
 
 cudaError_t make_cache_tmap(CUtensorMap* m, const void* base, int64_t rows, int D, int box_rows);
+cudaError_t set_smem_once(const void* func, size_t bytes);
 int num_sms_cached();
 
 template <int D, int BOX>
@@ -368,7 +375,7 @@ static cudaError_t launch_dense_db(const AttnParams& p, int64_t n_cache_pages, c
   e = make_cache_tmap(&tv, p.v_cache, rows, D, BOX);
   if (e != cudaSuccess) return e;
   const size_t smem = dense_layout(D).total + 1024;
-  e = cudaFuncSetAttribute(dense_kernel<D, BOX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  e = set_smem_once((const void*)dense_kernel<D, BOX>, smem);
   if (e != cudaSuccess) return e;
   const int grid = p.n_units < num_sms_cached() ? p.n_units : num_sms_cached();
   dense_kernel<D, BOX><<<grid, DN_THREADS, smem, st>>>(tk, tv, p);

@@ -17,6 +17,7 @@
 
 #include "blend.h"
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace blend {
 
@@ -147,6 +148,7 @@ __global__ void __launch_bounds__(128) generic_unit_kernel(AttnParams p) {
 
 // One warp per (merged token, q head); lanes own D/32 contiguous elements.
 __global__ void __launch_bounds__(256) merge_kernel(AttnParams p) {
+  ptx::pdl_wait();   // launched as a programmatic dependent of the streaming pass
   const int m = blockIdx.x;
   const int h = blockIdx.y * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -185,6 +187,8 @@ __global__ void __launch_bounds__(256) merge_kernel(AttnParams p) {
   if (lane == 0) p.lse[(int64_t)token * p.hq + h] = mx != -INFINITY ? (mx + log2f(tot)) * kLn2 : -INFINITY;
 }
 
+cudaError_t set_smem_once(const void* func, size_t bytes);
+
 size_t generic_smem_bytes(int D) {
   return sizeof(float) * ((size_t)GEN_ROWS * D * 2 + GEN_KT * (D + 1) + GEN_KT * D + GEN_ROWS * (GEN_KT + 1) +
                           4 * GEN_ROWS);
@@ -193,16 +197,24 @@ size_t generic_smem_bytes(int D) {
 cudaError_t launch_generic(const AttnParams& p, cudaStream_t st) {
   if (p.n_units <= 0) return cudaSuccess;
   size_t smem = generic_smem_bytes(p.d);
-  cudaError_t e = cudaFuncSetAttribute(generic_unit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = set_smem_once((const void*)generic_unit_kernel, smem);
   if (e != cudaSuccess) return e;
   generic_unit_kernel<<<p.n_units, 128, smem, st>>>(p);
   return cudaPeekAtLastError();
 }
 
-cudaError_t launch_merge(const AttnParams& p, cudaStream_t st) {
+cudaError_t launch_merge(const AttnParams& p, cudaStream_t st, bool pdl) {
   if (p.n_merge <= 0) return cudaSuccess;
-  merge_kernel<<<dim3(p.n_merge, (p.hq + 7) / 8), 256, 0, st>>>(p);
-  return cudaPeekAtLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.n_merge, (p.hq + 7) / 8);
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, merge_kernel, p);
 }
 
 }  // namespace blend

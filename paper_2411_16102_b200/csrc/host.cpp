@@ -124,7 +124,7 @@ int validate(const blend_build_args* a) {
     return fail(BLEND_EINVAL, "page_size must be a power of two in [16,128]");
   if (a->kv_dtype != BLEND_BF16 && a->kv_dtype != BLEND_F32) return fail(BLEND_EINVAL, "kv_dtype");
   if (a->rows_min < 0 || a->min_sep_len < -1 || a->force_class < 0 || a->force_class > 2 ||
-      a->split_tokens < 0 || a->num_sms < 0 || a->dense_split < 0)
+      a->split_tokens < 0 || a->num_sms < 0 || a->dense_split < 0 || a->fuse_merge < 0 || a->fuse_merge > 1)
     return fail(BLEND_EINVAL, "rows_min/min_sep_len/force_class/split_tokens/num_sms");
   if (a->n_req < 1) return fail(BLEND_EINVAL, "n_req must be >= 1");
   if (!a->tok_off || !a->tokens || !a->q_len || !a->prompt_len || !a->out_len)
@@ -616,7 +616,7 @@ int build_plan(blend_tree* t) {
     int n_stream = 0;
     while (j < srcs.size() && srcs[j].tok == srcs[i].tok) n_stream += srcs[j++].dense ? 0 : 1;
     if (j - i == 1) partmap[srcs[i].pm] = blend::PM_DIRECT;
-    else groups.push_back({i, j, n_stream == 1});
+    else groups.push_back({i, j, a.fuse_merge != 0 && n_stream == 1});
     i = j;
   }
   std::vector<int32_t> merge_tok, merge_off{0}, merge_rows;

@@ -22,6 +22,8 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
+#include <mutex>
+
 #include "blend.h"
 #include "common.cuh"
 #include "ptx.cuh"
@@ -64,6 +66,7 @@ __global__ void __launch_bounds__(ST_THREADS, 2)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
   uint64_t* empty = full + nstage;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  ptx::pdl_launch_dependents();
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < nstage; ++s) {
@@ -110,6 +113,7 @@ __global__ void __launch_bounds__(ST_THREADS, 2)
         }
       }
     }
+    ptx::pdl_wait();   // this grid completes only after the (overlapped) dense grid has completed
     return;
   }
 
@@ -324,6 +328,7 @@ __global__ void __launch_bounds__(ST_THREADS, 2)
     }
     ptx::named_bar_sync(1, 128);
   }
+  ptx::pdl_wait();
 }
 
 // ------------------------------------------------------------------ host side
@@ -343,8 +348,60 @@ static PFN_encodeTiled get_encode() {
   return fn;
 }
 
+// Host-side caches: tensor maps keyed by (base, rows, D, box) and per-kernel smem
+// attributes, so a steady-state blend_attention call only enqueues launches.
+namespace {
+struct TmapEntry {
+  const void* base;
+  int64_t rows;
+  int D, box;
+  CUtensorMap map;
+};
+std::mutex g_cache_mu;
+TmapEntry g_tmaps[32];
+int g_tmap_n = 0, g_tmap_next = 0;
+struct AttrEntry {
+  const void* func;
+  int device;
+  size_t bytes;
+};
+AttrEntry g_attrs[32];
+int g_attr_n = 0;
+}  // namespace
+
+cudaError_t set_smem_once(const void* func, size_t bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  for (int i = 0; i < g_attr_n; ++i)
+    if (g_attrs[i].func == func && g_attrs[i].device == dev && g_attrs[i].bytes >= bytes) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess && g_attr_n < 32) g_attrs[g_attr_n++] = {func, dev, bytes};
+  return e;
+}
+
+static cudaError_t encode_cache_tmap(CUtensorMap* m, const void* base, int64_t rows, int D, int box_rows);
+
 // 2-D view of a paged cache [pages*Hkv*ps rows][D] bf16, box {64 cols, box_rows}, 128B swizzle
 cudaError_t make_cache_tmap(CUtensorMap* m, const void* base, int64_t rows, int D, int box_rows) {
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  for (int i = 0; i < g_tmap_n; ++i) {
+    const TmapEntry& t = g_tmaps[i];
+    if (t.base == base && t.rows == rows && t.D == D && t.box == box_rows) {
+      *m = t.map;
+      return cudaSuccess;
+    }
+  }
+  cudaError_t e = encode_cache_tmap(m, base, rows, D, box_rows);
+  if (e != cudaSuccess) return e;
+  TmapEntry& t = g_tmaps[g_tmap_next];
+  t = {base, rows, D, box_rows, *m};
+  g_tmap_next = (g_tmap_next + 1) % 32;
+  if (g_tmap_n < 32) ++g_tmap_n;
+  return cudaSuccess;
+}
+
+static cudaError_t encode_cache_tmap(CUtensorMap* m, const void* base, int64_t rows, int D, int box_rows) {
   PFN_encodeTiled enc = get_encode();
   if (!enc) return cudaErrorNotSupported;
   cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)rows};
@@ -369,7 +426,7 @@ int num_sms_cached() {
 }
 
 template <int D>
-static cudaError_t launch_stream_d(const AttnParams& p, int64_t n_cache_pages, cudaStream_t st) {
+static cudaError_t launch_stream_d(const AttnParams& p, int64_t n_cache_pages, cudaStream_t st, bool overlap) {
   const int box_rows = p.ps < ST_KEYS ? p.ps : ST_KEYS;
   CUtensorMap tk, tv, tk16, tv16;
   const int64_t rows = n_cache_pages * p.hkv * p.ps;
@@ -387,20 +444,30 @@ static cudaError_t launch_stream_d(const AttnParams& p, int64_t n_cache_pages, c
   const int budget = ctas_per_sm == 2 ? 113 * 1024 : 227 * 1024;
   while (nstage > 2 && (int)stream_smem_layout(D, nstage).total + 1024 > budget) --nstage;
   const size_t smem = stream_smem_layout(D, nstage).total + 1024;
-  e = cudaFuncSetAttribute(stream_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  e = set_smem_once((const void*)stream_kernel<D>, smem);
   if (e != cudaSuccess) return e;
   const int slots = ctas_per_sm * num_sms_cached();
   const int grid = p.n_units < slots ? p.n_units : slots;
-  stream_kernel<D><<<grid, ST_THREADS, smem, st>>>(tk, tv, tk16, tv16, p, nstage, box_rows);
-  return cudaPeekAtLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(ST_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = overlap ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, stream_kernel<D>, tk, tv, tk16, tv16, p, nstage, box_rows);
 }
 
 cudaError_t launch_generic(const AttnParams& p, cudaStream_t st);
 
-cudaError_t launch_stream(const AttnParams& p, int64_t n_cache_pages, cudaStream_t st) {
+cudaError_t launch_stream(const AttnParams& p, int64_t n_cache_pages, cudaStream_t st, bool overlap) {
   if (p.n_units <= 0) return cudaSuccess;
   if (p.kv_f32) return launch_generic(p, st);
-  return p.d == 128 ? launch_stream_d<128>(p, n_cache_pages, st) : launch_stream_d<64>(p, n_cache_pages, st);
+  return p.d == 128 ? launch_stream_d<128>(p, n_cache_pages, st, overlap)
+                    : launch_stream_d<64>(p, n_cache_pages, st, overlap);
 }
 
 }  // namespace blend

@@ -193,3 +193,20 @@ def test_abi_errors():
         B.attention(db.q, db.k_cache, db.v_cache, db.plan, db.out, db.lse, db.ws,
                     n_cache_pages=db.n_cache_pages, path=7)
     assert e.value.status == B.EINVAL
+
+
+@pytest.mark.parametrize("fuse", [0, 1])
+@pytest.mark.parametrize("flags", [0, 1])
+def test_c2_fused_merge_and_overlap(fuse, flags):
+    """Fused merges (streaming unit merges the dense partials itself) and the PDL
+    overlap of the two passes give the same attention; serialised vs overlapped
+    runs of one plan are bitwise equal."""
+    w = W.c2_mmlu_decode()
+    db = device_batch(w, tree_kw=dict(fuse_merge=fuse))
+    db.run(flags=flags)
+    torch.cuda.synchronize()
+    _cmp(w, db)
+    first = db.out.clone()
+    db.run(flags=1 - flags)
+    torch.cuda.synchronize()
+    assert torch.equal(first, db.out)
