@@ -19,6 +19,7 @@ namespace blend {
 cudaError_t launch_generic(const AttnParams& p, cudaStream_t st);
 cudaError_t launch_merge(const AttnParams& p, cudaStream_t st, bool pdl);
 cudaError_t launch_stream(const AttnParams& p, int64_t n_cache_pages, cudaStream_t st, bool overlap);
+cudaError_t launch_streamw(const AttnParams& p, int64_t n_cache_pages, cudaStream_t st, bool overlap);
 cudaError_t launch_dense(const AttnParams& p, int64_t n_cache_pages, cudaStream_t st);
 }  // namespace blend
 
@@ -131,7 +132,8 @@ extern "C" int blend_attention(const blend_attn_args* a, void* stream) {
   ps_.n_units = (int32_t)pl.count[SEC_STREAM_UNITS];
   ps_.avg_entries = ps_.n_units > 0 ? (int32_t)(pl.count[SEC_COUNT + 1] / ps_.n_units) : 0;
   if (generic) e = launch_generic(ps_, st);
-  else e = launch_stream(ps_, a->n_cache_pages, st, overlap);
+  else if (n_merge_all != n_merge_unfused) e = launch_stream(ps_, a->n_cache_pages, st, overlap);   // fused merges
+  else e = launch_streamw(ps_, a->n_cache_pages, st, overlap);
   if (e != cudaSuccess) return cuda_fail(e);
 
   if (a->events[2]) cudaEventRecord((cudaEvent_t)a->events[2], st);

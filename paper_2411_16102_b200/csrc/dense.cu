@@ -97,9 +97,10 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   // register budget: warpgroup 0 (producer, MMA, allocator) needs few; the two softmax
-  // warpgroups keep a 128-score row in registers (48*128 + 232*256 = 64K registers)
+  // warpgroups keep a 128-score row in registers.  setmaxnreg only redistributes the
+  // CTA's own launch allocation (168 x 384 = 64512): 56*128 + 224*256 = 64512.
   if (warp < 4) {
-  ptx::setmaxnreg_dec<48>();
+  ptx::setmaxnreg_dec<56>();
   if (warp == 0) {
     // ===================== TMA producer =====================
     if (lane == 0) {
@@ -199,7 +200,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
     }
   }
   } else {
-    ptx::setmaxnreg_inc<232>();
+    ptx::setmaxnreg_inc<224>();
     // ===================== softmax / epilogue (tile t) =====================
     const int t = (warp - 4) >> 2;                    // 0 = tile A, 1 = tile B
     const int r = threadIdx.x - 128 - 128 * t;        // row within the tile = TMEM lane
@@ -255,7 +256,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         }
         ptx::mbar_wait(&s_full[t], sb & 1);
         ptx::tc_fence_after();
-        // the whole 128-score row in registers (softmax warps run with 232 registers)
+        // the whole 128-score row in registers (softmax warps run with 224 registers)
         float sv[DN_KB];
 #pragma unroll
         for (int c = 0; c < DN_KB / 32; ++c)
