@@ -513,14 +513,19 @@ int build_plan(blend_tree* t) {
 
   // ---- split-KV decisions (plan only; not part of the bit-exact contract)
   int64_t base_d = 0, base_s = 0, work_s = 0;
+  double flops_d = 0.0, bytes_s = 0.0;
+  const int kvb = a.kv_dtype == BLEND_BF16 ? 2 : 4;
   for (auto& it : items) {
     int64_t u = ntiles(it) * Hkv;
     int64_t kv = 0;
     for (auto& e : it.ents) kv += e.count;
-    if (it.dense) base_d += u;
-    else {
+    if (it.dense) {
+      base_d += u;
+      flops_d += 4.0 * a.head_dim * (double)it.toks.size() * a.num_q_heads * (double)kv;
+    } else {
       base_s += u;
       work_s += u * kv;
+      bytes_s += (double)u * kv * a.head_dim * 2 * kvb;
     }
   }
   int64_t chunk_s = INT64_MAX;
@@ -529,10 +534,18 @@ int build_plan(blend_tree* t) {
     chunk_s = std::max<int64_t>(512, (work_s + 8LL * num_sms - 1) / (8LL * num_sms));
     chunk_s = (chunk_s + 63) / 64 * 64;
   }
-  // dense split-KV: fill (at most) one wave of persistent CTAs without exceeding it
+  // dense split-KV: the dense grid overlaps the streaming grid (PDL), so give it the
+  // share of the SMs proportional to its estimated time (NEXT-1, the paper's resource
+  // overlap f = max, §2.4) and split its items until that share is filled.
+  // Rates are planning constants (~600 TFLOP/s dense, ~6 TB/s streaming on B200).
   int64_t dsplit = 1;
   if (a.dense_split > 0) dsplit = a.dense_split;
-  else if (base_d > 0 && base_d < num_sms) dsplit = num_sms / base_d;
+  else if (base_d > 0 && base_d < num_sms) {
+    const double t_d = flops_d / 600e12, t_s = bytes_s / 6e12;
+    const double share = t_d / (t_d + t_s);
+    const int64_t dense_sms = std::max<int64_t>(1, (int64_t)(share * num_sms + 0.5));
+    dsplit = std::max<int64_t>(1, dense_sms / base_d);
+  }
 
   std::vector<std::vector<int32_t>> split_b(items.size());   // entry boundaries per item
   for (size_t ii = 0; ii < items.size(); ++ii) {
