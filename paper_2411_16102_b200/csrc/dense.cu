@@ -14,6 +14,8 @@
 //                A/B from smem) into TMEM; O_t += P_t V with P_t read from TMEM
 //                (aliasing S_t) and V MN-major from smem; tcgen05.commit -> mbarriers
 //   warp 2       TMEM allocator (512 columns: S_A | S_B | O_A | O_B)
+//   warp 3       Q loader: gathers the next unit's 256 query rows (cp.async, 128B
+//                swizzle) as soon as the current unit's last QK has been issued
 //   warps 4..7   softmax / epilogue of tile A, warps 8..11 of tile B: thread =
 //                query row = TMEM lane; tcgen05.ld the S row, per-row causal mask,
 //                log2-domain online softmax with lazy O rescaling (only when the
@@ -86,7 +88,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       ptx::mbar_init(&s_full[t], 1);
       ptx::mbar_init(&p_full[t], 4);
       ptx::mbar_init(&o_done[t], 1);
-      ptx::mbar_init(&q_full[t], 4);
+      ptx::mbar_init(&q_full[t], 1);
     }
     ptx::mbar_init(q_empty, 1);
     ptx::fence_mbar_init();
@@ -131,6 +133,32 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         }
       }
     }
+  } else if (warp == 3) {
+    // ===================== Q loader: next unit's rows as soon as the last QK is issued =====
+    uint32_t gu = 0;
+    for (int ui = blockIdx.x; ui < p.n_units; ui += gridDim.x, ++gu) {
+      const Unit u = p.units[ui];
+      if (gu > 0) ptx::mbar_wait(q_empty, (gu - 1) & 1);
+      const int nrows = u.n_rows > 128 ? 256 : 128;
+      for (int row = lane; row < nrows; row += 32) {
+        uint8_t* qs = smem + ((row >> 7) ? L.q1 : L.q0);
+        const int r = row & 127;
+        if (row < u.n_rows) {
+          const RowInfo ri = row_info(p, u, row);
+          const __nv_bfloat16* src = reinterpret_cast<const __nv_bfloat16*>(p.q) + ((int64_t)ri.token * p.hq + ri.head) * D;
+#pragma unroll
+          for (int c = 0; c < D / 8; ++c) ptx::cp_async16(qs + (c / 8) * DN_CHUNK + ptx::sw128(r, c % 8), src + 8 * c);
+        } else {
+#pragma unroll
+          for (int c = 0; c < D / 8; ++c)
+            *reinterpret_cast<uint4*>(qs + (c / 8) * DN_CHUNK + ptx::sw128(r, c % 8)) = make_uint4(0, 0, 0, 0);
+        }
+      }
+      ptx::cp_async_wait_all();
+      ptx::fence_proxy_async_smem();   // generic-proxy smem writes -> visible to the tensor core
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&q_full[0]);
+    }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
     if (lane == 0) {
@@ -143,7 +171,6 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         const int nb = (u.entry_end - u.entry_begin + EPB - 1) / EPB;
         const int ntile = u.n_rows > 128 ? 2 : 1;
         ptx::mbar_wait(&q_full[0], gu & 1);
-        ptx::mbar_wait(&q_full[1], gu & 1);
         ptx::tc_fence_after();
         uint32_t s = kit % NS;
         ptx::mbar_wait(&kv_full[s], (kit / NS) & 1);
@@ -159,6 +186,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
           }
           ptx::umma_commit(&s_full[t]);
         }
+        if (nb == 1) ptx::umma_commit(q_empty);   // last QK of the unit issued: Q may be reloaded
         for (int j = 0; j < nb; ++j) {
           const uint32_t vst = kst + CH * DN_CHUNK;
           const uint32_t s_cur = s;
@@ -190,10 +218,10 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
               ptx::umma_commit(&o_done[t]);
             }
           }
+          if (j + 2 == nb) ptx::umma_commit(q_empty);   // QK(nb-1) of every tile issued
           ptx::umma_commit(&kv_empty[s_cur]);
           kst = kst_next;
         }
-        ptx::umma_commit(q_empty);
         kit += nb;
         ++gu;
       }
@@ -206,7 +234,6 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
     const int r = threadIdx.x - 128 - 128 * t;        // row within the tile = TMEM lane
     const uint32_t lane_base = (uint32_t)(((warp - 4) & 3) * 32) << 16;
     const uint32_t col_s = t * DN_KB, col_o = 2 * DN_KB + t * D;
-    uint8_t* qs = smem + (t ? L.q1 : L.q0);
     uint32_t gu = 0, sb = 0, uo = 0;                  // unit, block and tile-unit counters
     for (int ui = blockIdx.x; ui < p.n_units; ui += gridDim.x) {
       const Unit u = p.units[ui];
@@ -221,20 +248,6 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         head = ri.head;
         tgt = row_target(p, u, ri.tl);
       }
-      // ---- Q row -> smem (K-major, 128B swizzle) once the previous unit's MMAs are done
-      if (gu > 0) ptx::mbar_wait(q_empty, (gu - 1) & 1);
-      if (active) {
-        const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(p.q) +
-                                                          ((int64_t)token * p.hq + head) * D);
-#pragma unroll
-        for (int c = 0; c < D / 8; ++c) {
-          uint4 v = row < u.n_rows ? __ldg(src + c) : make_uint4(0, 0, 0, 0);
-          *reinterpret_cast<uint4*>(qs + (c / 8) * DN_CHUNK + ptx::sw128(r, c % 8)) = v;
-        }
-        ptx::fence_proxy_async_smem();
-      }
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&q_full[t]);
       ++gu;
       if (!active) continue;
 

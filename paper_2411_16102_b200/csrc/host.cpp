@@ -537,14 +537,15 @@ int build_plan(blend_tree* t) {
   // dense split-KV: the dense grid overlaps the streaming grid (PDL), so give it the
   // share of the SMs proportional to its estimated time (NEXT-1, the paper's resource
   // overlap f = max, §2.4) and split its items until that share is filled.
-  // Rates are planning constants (~600 TFLOP/s dense, ~6 TB/s streaming on B200).
+  // Rates are planning constants measured on B200 for the two kernels (~250 TFLOP/s for
+  // the short dense units this split targets, ~6 TB/s streaming).
   int64_t dsplit = 1;
   if (a.dense_split > 0) dsplit = a.dense_split;
   else if (base_d > 0 && base_d < num_sms) {
-    const double t_d = flops_d / 600e12, t_s = bytes_s / 6e12;
+    const double t_d = flops_d / 250e12, t_s = bytes_s / 6e12;
     const double share = t_d / (t_d + t_s);
     const int64_t dense_sms = std::max<int64_t>(1, (int64_t)(share * num_sms + 0.5));
-    dsplit = std::max<int64_t>(1, dense_sms / base_d);
+    dsplit = std::max<int64_t>(1, (dense_sms + base_d / 2) / base_d);
   }
 
   std::vector<std::vector<int32_t>> split_b(items.size());   // entry boundaries per item
