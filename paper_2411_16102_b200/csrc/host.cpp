@@ -546,6 +546,33 @@ int build_plan(blend_tree* t) {
     const double share = t_d / (t_d + t_s);
     const int64_t dense_sms = std::max<int64_t>(1, (int64_t)(share * num_sms + 0.5));
     dsplit = std::max<int64_t>(1, (dense_sms + base_d / 2) / base_d);
+  } else if (base_d > 0) {
+    // more units than SMs: split long items so the last wave of persistent CTAs is full
+    // (e.g. 256 units of a 31K-token document on 148 SMs -> 4 splits, 99% wave fill)
+    int64_t n_dense_items = 0, kv_dense = 0;
+    for (auto& it : items)
+      if (it.dense) {
+        ++n_dense_items;
+        for (auto& e : it.ents) kv_dense += e.count;
+      }
+    const int64_t avg_kv = kv_dense / std::max<int64_t>(1, n_dense_items);
+    auto fill = [&](int64_t s_) {   // wave fill with the per-item cap min(s, kv / 256) used below
+      int64_t units = 0;
+      for (auto& it : items)
+        if (it.dense) {
+          int64_t kv = 0;
+          for (auto& e : it.ents) kv += e.count;
+          units += ntiles(it) * Hkv * std::max<int64_t>(1, std::min<int64_t>(s_, kv / 256));
+        }
+      const int64_t waves = (units + num_sms - 1) / num_sms;
+      return (double)units / (double)(waves * num_sms);
+    };
+    double best = fill(1);
+    for (int64_t s_ = 2; s_ <= 8 && avg_kv / s_ >= 2048; ++s_)
+      if (fill(s_) > best + 0.02) {
+        best = fill(s_);
+        dsplit = s_;
+      }
   }
 
   std::vector<std::vector<int32_t>> split_b(items.size());   // entry boundaries per item
