@@ -275,17 +275,18 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         for (int c = 0; c < DN_KB / 32; ++c)
           ptx::tmem_ld32(tmem + lane_base + col_s + c * 32, reinterpret_cast<uint32_t*>(sv + c * 32));
         ptx::tmem_wait_ld();
-        float mx = -INFINITY;
-        if (full_vis) {
+        if (!full_vis) {
 #pragma unroll
-          for (int k = 0; k < DN_KB; ++k) mx = fmaxf(mx, sv[k]);
-        } else {
-#pragma unroll
-          for (int k = 0; k < DN_KB; ++k) {
-            sv[k] = (k % BOX) < vis[k / BOX] ? sv[k] : -INFINITY;
-            mx = fmaxf(mx, sv[k]);
-          }
+          for (int k = 0; k < DN_KB; ++k) sv[k] = (k % BOX) < vis[k / BOX] ? sv[k] : -INFINITY;
         }
+        // 8 independent max chains (a single 128-long FMNMX chain would cost ~512 cycles)
+        float mxv[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) mxv[i] = sv[i];
+#pragma unroll
+        for (int k = 8; k < DN_KB; ++k) mxv[k & 7] = fmaxf(mxv[k & 7], sv[k]);
+        const float mx = fmaxf(fmaxf(fmaxf(mxv[0], mxv[1]), fmaxf(mxv[2], mxv[3])),
+                               fmaxf(fmaxf(mxv[4], mxv[5]), fmaxf(mxv[6], mxv[7])));
         const float mx2 = mx * p.scale_log2;
         const bool need = mx2 > m_ref + DN_RESCALE_T;
         // s_full(j) certifies PV(j-1): O may be rescaled now
@@ -306,7 +307,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
           m_ref = mx2;
         }
         const float m_use = m_ref == -INFINITY ? 0.f : m_ref;
-        float lsum = 0.f;
+        float ls[4] = {0.f, 0.f, 0.f, 0.f};   // independent partial sums (ILP)
         // P = exp2(s*scale - m): 3 of every 4 on the MUFU pipe, 1 of 4 as a polynomial on
         // the FMA pipe (the two pipes run concurrently); bf16 pairs -> TMEM columns [0, 64)
 #pragma unroll
@@ -319,12 +320,12 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
             const float x1 = fmaf(sv[key + 1], p.scale_log2, -m_use);
             const float p0 = ptx::ex2(x0);
             const float p1 = (k & 1) ? ptx::exp2_poly(x1) : ptx::ex2(x1);
-            lsum += p0 + p1;
+            ls[k & 3] += p0 + p1;
             pk[k] = ptx::pack_bf16(p0, p1);
           }
           ptx::tmem_st16(tmem + lane_base + col_s + c * 16, pk);   // keys 32c.. -> columns 16c..
         }
-        l += lsum;
+        l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
         __syncwarp();
