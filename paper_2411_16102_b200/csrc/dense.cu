@@ -35,8 +35,9 @@
 namespace blend {
 
 constexpr int DN_THREADS = 384;
-constexpr int DN_KB = 128;               // keys per block (UMMA N of QK^T, K of PV)
-constexpr int DN_CHUNK = 128 * 128;      // 128 rows x 128 B (one 64-column chunk)
+constexpr int DN_KB = 64;                // keys per block (UMMA N of QK^T, K of PV)
+constexpr int DN_QCHUNK = 128 * 128;     // Q: 128 rows x 128 B (one 64-column chunk)
+constexpr int DN_KCHUNK = DN_KB * 128;   // K/V: 64 rows x 128 B
 constexpr uint32_t DN_TMEM_COLS = 512;
 constexpr float DN_RESCALE_T = 8.0f;     // lazy-rescale threshold (log2 units)
 
@@ -49,12 +50,12 @@ __host__ __device__ inline DenseSmem dense_layout(int D) {
   DenseSmem L;
   const int CH = D / 64;
   L.q0 = 0;
-  L.q1 = CH * DN_CHUNK;
-  L.stage0 = 2 * CH * DN_CHUNK;
-  L.stage_stride = 2 * CH * DN_CHUNK;
-  L.nstage = D == 128 ? 2 : 4;
+  L.q1 = CH * DN_QCHUNK;
+  L.stage0 = 2 * CH * DN_QCHUNK;
+  L.stage_stride = 2 * CH * DN_KCHUNK;   // K chunks then V chunks
+  L.nstage = D == 128 ? 4 : 8;
   L.bar = L.stage0 + L.nstage * L.stage_stride;
-  L.total = L.bar + 256;
+  L.total = L.bar + 512;
   return L;
 }
 
@@ -62,20 +63,20 @@ template <int D, int BOX>
 __global__ void __launch_bounds__(DN_THREADS, 1)
     dense_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv, AttnParams p) {
   constexpr int CH = D / 64;
-  constexpr int EPB = DN_KB / BOX;      // page entries per 128-key block
+  constexpr int EPB = DN_KB / BOX;      // page entries per 64-key block
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const DenseSmem L = dense_layout(D);
   const int NS = L.nstage;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar);
-  uint64_t* kv_full = bars;            // [NS <= 4]
-  uint64_t* kv_empty = bars + 4;       // [NS]
-  uint64_t* s_full = bars + 8;         // [2] per tile
-  uint64_t* p_full = bars + 10;        // [2]
-  uint64_t* o_done = bars + 12;        // [2]
-  uint64_t* q_full = bars + 14;        // [2]
-  uint64_t* q_empty = bars + 16;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+  uint64_t* kv_full = bars;            // [NS <= 8]
+  uint64_t* kv_empty = bars + 8;       // [NS]
+  uint64_t* s_full = bars + 16;        // [tile][buffer]
+  uint64_t* p_full = bars + 20;        // [tile][buffer]
+  uint64_t* o_done = bars + 24;        // [tile]
+  uint64_t* q_full = bars + 26;
+  uint64_t* q_empty = bars + 27;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 28);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   ptx::pdl_launch_dependents();   // the streaming pass may start on SMs this grid leaves free
@@ -84,12 +85,13 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       ptx::mbar_init(&kv_full[s], 1);
       ptx::mbar_init(&kv_empty[s], 1);
     }
-    for (int t = 0; t < 2; ++t) {
-      ptx::mbar_init(&s_full[t], 1);
-      ptx::mbar_init(&p_full[t], 4);
-      ptx::mbar_init(&o_done[t], 1);
-      ptx::mbar_init(&q_full[t], 1);
+    for (int i = 0; i < 4; ++i) {
+      ptx::mbar_init(&s_full[i], 1);
+      ptx::mbar_init(&p_full[i], 4);
     }
+    ptx::mbar_init(&o_done[0], 1);
+    ptx::mbar_init(&o_done[1], 1);
+    ptx::mbar_init(q_full, 1);
     ptx::mbar_init(q_empty, 1);
     ptx::fence_mbar_init();
   }
@@ -98,13 +100,15 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // register budget: warpgroup 0 (producer, MMA, allocator) needs few; the two softmax
-  // warpgroups keep a 128-score row in registers.  setmaxnreg only redistributes the
-  // CTA's own launch allocation (168 x 384 = 64512): 56*128 + 224*256 = 64512.
+  // TMEM columns: S[tile][buffer] 64 fp32 columns each at tile*128 + buffer*64 (P, bf16
+  // pairs, aliases the first 32 columns of its S buffer); O[tile] at 256 + tile*D.
+  // register budget: warpgroup 0 (producer, MMA, allocator, Q loader) needs few; the
+  // softmax warpgroups get the rest of the CTA's launch allocation (168 x 384 = 64512 =
+  // 56*128 + 224*256; setmaxnreg only redistributes the CTA's own registers).
   if (warp < 4) {
   ptx::setmaxnreg_dec<56>();
   if (warp == 0) {
-    // ===================== TMA producer =====================
+    // ===================== TMA producer: 64-key K/V blocks into the stage ring =====================
     if (lane == 0) {
       ptx::tma_prefetch_desc(&tmk);
       ptx::tma_prefetch_desc(&tmv);
@@ -116,8 +120,8 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
           const uint32_t s = kit % NS, ph = (kit / NS) & 1;
           ptx::mbar_wait(&kv_empty[s], ph ^ 1);
           uint8_t* kst = smem + L.stage0 + s * L.stage_stride;
-          uint8_t* vst = kst + CH * DN_CHUNK;
-          ptx::mbar_arrive_expect_tx(&kv_full[s], 2u * CH * DN_CHUNK);
+          uint8_t* vst = kst + CH * DN_KCHUNK;
+          ptx::mbar_arrive_expect_tx(&kv_full[s], 2u * CH * DN_KCHUNK);
 #pragma unroll
           for (int i = 0; i < EPB; ++i) {
             int e = u.entry_begin + j * EPB + i;
@@ -126,15 +130,15 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
             const int32_t y = (en.page * p.hkv + u.kvh) * p.ps + en.row_off;
 #pragma unroll
             for (int c = 0; c < CH; ++c) {
-              ptx::tma_load_2d(kst + c * DN_CHUNK + i * BOX * 128, &tmk, &kv_full[s], c * 64, y);
-              ptx::tma_load_2d(vst + c * DN_CHUNK + i * BOX * 128, &tmv, &kv_full[s], c * 64, y);
+              ptx::tma_load_2d(kst + c * DN_KCHUNK + i * BOX * 128, &tmk, &kv_full[s], c * 64, y);
+              ptx::tma_load_2d(vst + c * DN_KCHUNK + i * BOX * 128, &tmv, &kv_full[s], c * 64, y);
             }
           }
         }
       }
     }
   } else if (warp == 3) {
-    // ===================== Q loader: next unit's rows as soon as the last QK is issued =====
+    // ===================== Q loader: next unit's rows as soon as its last QK is issued =====
     uint32_t gu = 0;
     for (int ui = blockIdx.x; ui < p.n_units; ui += gridDim.x, ++gu) {
       const Unit u = p.units[ui];
@@ -145,82 +149,81 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         const int r = row & 127;
         if (row < u.n_rows) {
           const RowInfo ri = row_info(p, u, row);
-          const __nv_bfloat16* src = reinterpret_cast<const __nv_bfloat16*>(p.q) + ((int64_t)ri.token * p.hq + ri.head) * D;
+          const __nv_bfloat16* src =
+              reinterpret_cast<const __nv_bfloat16*>(p.q) + ((int64_t)ri.token * p.hq + ri.head) * D;
 #pragma unroll
-          for (int c = 0; c < D / 8; ++c) ptx::cp_async16(qs + (c / 8) * DN_CHUNK + ptx::sw128(r, c % 8), src + 8 * c);
+          for (int c = 0; c < D / 8; ++c)
+            ptx::cp_async16(qs + (c / 8) * DN_QCHUNK + ptx::sw128(r, c % 8), src + 8 * c);
         } else {
 #pragma unroll
           for (int c = 0; c < D / 8; ++c)
-            *reinterpret_cast<uint4*>(qs + (c / 8) * DN_CHUNK + ptx::sw128(r, c % 8)) = make_uint4(0, 0, 0, 0);
+            *reinterpret_cast<uint4*>(qs + (c / 8) * DN_QCHUNK + ptx::sw128(r, c % 8)) = make_uint4(0, 0, 0, 0);
         }
       }
       ptx::cp_async_wait_all();
       ptx::fence_proxy_async_smem();   // generic-proxy smem writes -> visible to the tensor core
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&q_full[0]);
+      if (lane == 0) ptx::mbar_arrive(q_full);
     }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
+    // Per unit: QK(0), QK(1) for every tile, then for j = 0..nb-1 and each tile:
+    //   wait P_t(j) -> PV_t(j) (P from TMEM) -> commit o_done_t -> QK_t(j+2) into the
+    //   S buffer PV_t(j) just consumed (MMAs execute in issue order) -> commit s_full.
     if (lane == 0) {
       constexpr uint32_t IDESC_QK = ptx::umma_idesc_bf16(128, DN_KB, 0, 0);
       constexpr uint32_t IDESC_PV = ptx::umma_idesc_bf16(128, D, 0, 1);
       const uint32_t q_addr0 = ptx::smem_u32(smem + L.q0), q_addr1 = ptx::smem_u32(smem + L.q1);
-      uint32_t kit = 0, gu = 0, pb0 = 0, pb1 = 0;
+      uint32_t kit = 0, gu = 0;
+      uint32_t pb[4] = {0, 0, 0, 0};    // completions consumed per p_full[tile][buffer]
       for (int ui = blockIdx.x; ui < p.n_units; ui += gridDim.x) {
         const Unit u = p.units[ui];
         const int nb = (u.entry_end - u.entry_begin + EPB - 1) / EPB;
         const int ntile = u.n_rows > 128 ? 2 : 1;
-        ptx::mbar_wait(&q_full[0], gu & 1);
-        ptx::tc_fence_after();
-        uint32_t s = kit % NS;
-        ptx::mbar_wait(&kv_full[s], (kit / NS) & 1);
-        ptx::tc_fence_after();
-        uint32_t kst = ptx::smem_u32(smem + L.stage0 + s * L.stage_stride);
-        for (int t = 0; t < ntile; ++t) {
+        auto stage_addr = [&](int j) { return ptx::smem_u32(smem + L.stage0 + ((kit + j) % NS) * L.stage_stride); };
+        auto wait_kv = [&](int j) {
+          ptx::mbar_wait(&kv_full[(kit + j) % NS], ((kit + j) / NS) & 1);
+          ptx::tc_fence_after();
+        };
+        auto issue_qk = [&](int t, int j, uint32_t kst) {
           const uint32_t qa = t ? q_addr1 : q_addr0;
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t off = (kk / 4) * DN_CHUNK + (kk % 4) * 32;
-            ptx::umma_f16(tmem + t * DN_KB, ptx::umma_desc_sw128(qa + off, 16, 1024),
-                          ptx::umma_desc_sw128(kst + off, 16, 1024), IDESC_QK, kk > 0);
-          }
-          ptx::umma_commit(&s_full[t]);
+          for (int kk = 0; kk < D / 16; ++kk)
+            ptx::umma_f16(tmem + t * 128 + (j & 1) * DN_KB,
+                          ptx::umma_desc_sw128(qa + (kk / 4) * DN_QCHUNK + (kk % 4) * 32, 16, 1024),
+                          ptx::umma_desc_sw128(kst + (kk / 4) * DN_KCHUNK + (kk % 4) * 32, 16, 1024), IDESC_QK,
+                          kk > 0);
+          ptx::umma_commit(&s_full[t * 2 + (j & 1)]);
+        };
+        ptx::mbar_wait(q_full, gu & 1);
+        ptx::tc_fence_after();
+        for (int j = 0; j < 2 && j < nb; ++j) {
+          wait_kv(j);
+          const uint32_t kst = stage_addr(j);
+          for (int t = 0; t < ntile; ++t) issue_qk(t, j, kst);
         }
-        if (nb == 1) ptx::umma_commit(q_empty);   // last QK of the unit issued: Q may be reloaded
+        if (nb <= 2) ptx::umma_commit(q_empty);   // every QK of the unit issued: Q may be reloaded
         for (int j = 0; j < nb; ++j) {
-          const uint32_t vst = kst + CH * DN_CHUNK;
-          const uint32_t s_cur = s;
-          uint32_t kst_next = 0;
-          if (j + 1 < nb) {
-            s = (kit + j + 1) % NS;
-            ptx::mbar_wait(&kv_full[s], ((kit + j + 1) / NS) & 1);
-            kst_next = ptx::smem_u32(smem + L.stage0 + s * L.stage_stride);
+          const uint32_t vst = stage_addr(j) + CH * DN_KCHUNK;
+          uint32_t kst2 = 0;
+          if (j + 2 < nb) {
+            wait_kv(j + 2);
+            kst2 = stage_addr(j + 2);
           }
           for (int t = 0; t < ntile; ++t) {
-            if (t == 0) ptx::mbar_wait(&p_full[0], (pb0++) & 1);
-            else ptx::mbar_wait(&p_full[1], (pb1++) & 1);
+            const int pi = t * 2 + (j & 1);
+            ptx::mbar_wait(&p_full[pi], (pb[pi]++) & 1);
             ptx::tc_fence_after();
 #pragma unroll
             for (int kk = 0; kk < DN_KB / 16; ++kk)
-              ptx::umma_f16_ts(tmem + 2 * DN_KB + t * D, tmem + t * DN_KB + kk * 8,
-                               ptx::umma_desc_sw128(vst + kk * 16 * 128, DN_CHUNK, 1024), IDESC_PV,
+              ptx::umma_f16_ts(tmem + 256 + t * D, tmem + t * 128 + (j & 1) * DN_KB + kk * 8,
+                               ptx::umma_desc_sw128(vst + kk * 16 * 128, DN_KCHUNK, 1024), IDESC_PV,
                                (j > 0 || kk > 0) ? 1u : 0u);
-            if (j + 1 < nb) {
-              const uint32_t qa = t ? q_addr1 : q_addr0;
-#pragma unroll
-              for (int kk = 0; kk < D / 16; ++kk) {
-                const uint32_t off = (kk / 4) * DN_CHUNK + (kk % 4) * 32;
-                ptx::umma_f16(tmem + t * DN_KB, ptx::umma_desc_sw128(qa + off, 16, 1024),
-                              ptx::umma_desc_sw128(kst_next + off, 16, 1024), IDESC_QK, kk > 0);
-              }
-              ptx::umma_commit(&s_full[t]);
-            } else {
-              ptx::umma_commit(&o_done[t]);
-            }
+            ptx::umma_commit(&o_done[t]);
+            if (j + 2 < nb) issue_qk(t, j + 2, kst2);
           }
-          if (j + 2 == nb) ptx::umma_commit(q_empty);   // QK(nb-1) of every tile issued
-          ptx::umma_commit(&kv_empty[s_cur]);
-          kst = kst_next;
+          if (j + 3 == nb) ptx::umma_commit(q_empty);   // QK(nb-1) of every tile issued
+          ptx::umma_commit(&kv_empty[(kit + j) % NS]);
         }
         kit += nb;
         ++gu;
@@ -233,12 +236,13 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
     const int t = (warp - 4) >> 2;                    // 0 = tile A, 1 = tile B
     const int r = threadIdx.x - 128 - 128 * t;        // row within the tile = TMEM lane
     const uint32_t lane_base = (uint32_t)(((warp - 4) & 3) * 32) << 16;
-    const uint32_t col_s = t * DN_KB, col_o = 2 * DN_KB + t * D;
-    uint32_t gu = 0, sb = 0, uo = 0;                  // unit, block and tile-unit counters
+    const uint32_t col_o = 256 + t * D;
+    uint32_t sb = 0;                                  // blocks of this tile processed so far
+    uint32_t scnt[2] = {0, 0};                        // s_full completions consumed per S buffer
     for (int ui = blockIdx.x; ui < p.n_units; ui += gridDim.x) {
       const Unit u = p.units[ui];
       const int nb = (u.entry_end - u.entry_begin + EPB - 1) / EPB;
-      const bool active = t == 0 || u.n_rows > 128;
+      if (t == 1 && u.n_rows <= 128) continue;       // tile B idle for this unit
       const int row = 128 * t + r;                    // row within the unit
       int32_t pos = INT32_MIN, token = 0, head = 0, tgt = PM_SKIP;
       if (row < u.n_rows) {
@@ -248,11 +252,10 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         head = ri.head;
         tgt = row_target(p, u, ri.tl);
       }
-      ++gu;
-      if (!active) continue;
-
       float m_ref = -INFINITY, l = 0.f;
       for (int j = 0; j < nb; ++j, ++sb) {
+        const int buf = j & 1;
+        const uint32_t col_s = t * 128 + buf * DN_KB;
         int vis[EPB];
         bool full_vis = true;
 #pragma unroll
@@ -267,19 +270,16 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
           vis[i] = v;
           full_vis = full_vis && (v == BOX);
         }
-        ptx::mbar_wait(&s_full[t], sb & 1);
+        ptx::mbar_wait(&s_full[t * 2 + buf], (scnt[buf]++) & 1);   // per-buffer completion count
         ptx::tc_fence_after();
-        // the whole 128-score row in registers (softmax warps run with 224 registers)
         float sv[DN_KB];
-#pragma unroll
-        for (int c = 0; c < DN_KB / 32; ++c)
-          ptx::tmem_ld32(tmem + lane_base + col_s + c * 32, reinterpret_cast<uint32_t*>(sv + c * 32));
+        ptx::tmem_ld32(tmem + lane_base + col_s, reinterpret_cast<uint32_t*>(sv));
+        ptx::tmem_ld32(tmem + lane_base + col_s + 32, reinterpret_cast<uint32_t*>(sv + 32));
         ptx::tmem_wait_ld();
         if (!full_vis) {
 #pragma unroll
           for (int k = 0; k < DN_KB; ++k) sv[k] = (k % BOX) < vis[k / BOX] ? sv[k] : -INFINITY;
         }
-        // 8 independent max chains (a single 128-long FMNMX chain would cost ~512 cycles)
         float mxv[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) mxv[i] = sv[i];
@@ -289,8 +289,10 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
                                fmaxf(fmaxf(mxv[4], mxv[5]), fmaxf(mxv[6], mxv[7])));
         const float mx2 = mx * p.scale_log2;
         const bool need = mx2 > m_ref + DN_RESCALE_T;
-        // s_full(j) certifies PV(j-1): O may be rescaled now
         if (j > 0 && __any_sync(0xffffffffu, need)) {
+          // O holds PV up to block j-1: wait for it (o_done is at most one phase ahead)
+          ptx::mbar_wait(&o_done[t], (sb - 1) & 1);
+          ptx::tc_fence_after();
           const float alpha = need ? ptx::ex2(m_ref - mx2) : 1.f;
 #pragma unroll 1
           for (int c = 0; c < D / 32; ++c) {
@@ -307,9 +309,9 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
           m_ref = mx2;
         }
         const float m_use = m_ref == -INFINITY ? 0.f : m_ref;
-        float ls[4] = {0.f, 0.f, 0.f, 0.f};   // independent partial sums (ILP)
+        float ls[4] = {0.f, 0.f, 0.f, 0.f};
         // P = exp2(s*scale - m): 3 of every 4 on the MUFU pipe, 1 of 4 as a polynomial on
-        // the FMA pipe (the two pipes run concurrently); bf16 pairs -> TMEM columns [0, 64)
+        // the FMA pipe; bf16 pairs -> the first 32 TMEM columns of this S buffer
 #pragma unroll
         for (int c = 0; c < DN_KB / 32; ++c) {
           uint32_t pk[16];
@@ -323,17 +325,16 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
             ls[k & 3] += p0 + p1;
             pk[k] = ptx::pack_bf16(p0, p1);
           }
-          ptx::tmem_st16(tmem + lane_base + col_s + c * 16, pk);   // keys 32c.. -> columns 16c..
+          ptx::tmem_st16(tmem + lane_base + col_s + c * 16, pk);
         }
         l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&p_full[t]);
+        if (lane == 0) ptx::mbar_arrive(&p_full[t * 2 + buf]);
       }
-      // ---- epilogue
-      ptx::mbar_wait(&o_done[t], uo & 1);
-      ++uo;
+      // ---- epilogue: PV of the unit's last block done
+      ptx::mbar_wait(&o_done[t], (sb - 1) & 1);
       ptx::tc_fence_after();
       const float m_use = m_ref == -INFINITY ? 0.f : m_ref;
       const float inv = l > 0.f ? 1.f / l : 0.f;
