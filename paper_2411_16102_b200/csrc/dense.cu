@@ -73,10 +73,10 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
   uint64_t* kv_empty = bars + 8;       // [NS]
   uint64_t* s_full = bars + 16;        // [tile][buffer]
   uint64_t* p_full = bars + 20;        // [tile][buffer]
-  uint64_t* o_done = bars + 24;        // [tile]
-  uint64_t* q_full = bars + 26;
-  uint64_t* q_empty = bars + 27;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 28);
+  uint64_t* o_done = bars + 24;        // [tile][buffer]: PV of a block that used this S buffer
+  uint64_t* q_full = bars + 28;
+  uint64_t* q_empty = bars + 29;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 30);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   ptx::pdl_launch_dependents();   // the streaming pass may start on SMs this grid leaves free
@@ -88,9 +88,8 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
     for (int i = 0; i < 4; ++i) {
       ptx::mbar_init(&s_full[i], 1);
       ptx::mbar_init(&p_full[i], 4);
+      ptx::mbar_init(&o_done[i], 1);
     }
-    ptx::mbar_init(&o_done[0], 1);
-    ptx::mbar_init(&o_done[1], 1);
     ptx::mbar_init(q_full, 1);
     ptx::mbar_init(q_empty, 1);
     ptx::fence_mbar_init();
@@ -109,13 +108,29 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
   ptx::setmaxnreg_dec<56>();
   if (warp == 0) {
     // ===================== TMA producer: 64-key K/V blocks into the stage ring =====================
+    // The entries of the next block (and the next unit's header) are loaded one step
+    // ahead, so a freed stage is refilled without waiting on dependent global loads.
     if (lane == 0) {
       ptx::tma_prefetch_desc(&tmk);
       ptx::tma_prefetch_desc(&tmv);
+      const int4* ents = reinterpret_cast<const int4*>(p.entries);
       uint32_t kit = 0;
-      for (int ui = blockIdx.x; ui < p.n_units; ui += gridDim.x) {
-        const Unit u = p.units[ui];
+      int ui = blockIdx.x;
+      Unit u = ui < p.n_units ? p.units[ui] : Unit{};
+      int4 cur[EPB];
+      auto load_block = [&](const Unit& un, int j) {
+#pragma unroll
+        for (int i = 0; i < EPB; ++i) {
+          int e = un.entry_begin + j * EPB + i;
+          if (e >= un.entry_end) e = un.entry_begin;   // pad the last block (masked)
+          cur[i] = ents[e];
+        }
+      };
+      if (ui < p.n_units) load_block(u, 0);
+      while (ui < p.n_units) {
         const int nb = (u.entry_end - u.entry_begin + EPB - 1) / EPB;
+        const int ui_next = ui + gridDim.x;
+        const Unit un = ui_next < p.n_units ? p.units[ui_next] : Unit{};
         for (int j = 0; j < nb; ++j, ++kit) {
           const uint32_t s = kit % NS, ph = (kit / NS) & 1;
           ptx::mbar_wait(&kv_empty[s], ph ^ 1);
@@ -124,17 +139,18 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
           ptx::mbar_arrive_expect_tx(&kv_full[s], 2u * CH * DN_KCHUNK);
 #pragma unroll
           for (int i = 0; i < EPB; ++i) {
-            int e = u.entry_begin + j * EPB + i;
-            if (e >= u.entry_end) e = u.entry_begin;   // pad the last block (masked)
-            const KvEntry en = p.entries[e];
-            const int32_t y = (en.page * p.hkv + u.kvh) * p.ps + en.row_off;
+            const int32_t y = (cur[i].x * p.hkv + u.kvh) * p.ps + cur[i].y;   // {page, row_off, pos0, count}
 #pragma unroll
             for (int c = 0; c < CH; ++c) {
               ptx::tma_load_2d(kst + c * DN_KCHUNK + i * BOX * 128, &tmk, &kv_full[s], c * 64, y);
               ptx::tma_load_2d(vst + c * DN_KCHUNK + i * BOX * 128, &tmv, &kv_full[s], c * 64, y);
             }
           }
+          if (j + 1 < nb) load_block(u, j + 1);
+          else if (ui_next < p.n_units) load_block(un, 0);
         }
+        ui = ui_next;
+        u = un;
       }
     }
   } else if (warp == 3) {
@@ -219,7 +235,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
               ptx::umma_f16_ts(tmem + 256 + t * D, tmem + t * 128 + (j & 1) * DN_KB + kk * 8,
                                ptx::umma_desc_sw128(vst + kk * 16 * 128, DN_KCHUNK, 1024), IDESC_PV,
                                (j > 0 || kk > 0) ? 1u : 0u);
-            ptx::umma_commit(&o_done[t]);
+            ptx::umma_commit(&o_done[pi]);
             if (j + 2 < nb) issue_qk(t, j + 2, kst2);
           }
           if (j + 3 == nb) ptx::umma_commit(q_empty);   // QK(nb-1) of every tile issued
@@ -290,8 +306,11 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         const float mx2 = mx * p.scale_log2;
         const bool need = mx2 > m_ref + DN_RESCALE_T;
         if (j > 0 && __any_sync(0xffffffffu, need)) {
-          // O holds PV up to block j-1: wait for it (o_done is at most one phase ahead)
-          ptx::mbar_wait(&o_done[t], (sb - 1) & 1);
+          // O holds PV up to block j-1: wait for it.  Parity is unambiguous because the
+          // previous completion on this barrier (PV(j-3)) is certified by s_full(j-1) and
+          // PV(j+1) cannot be issued before this block's P.
+          const int pb_ = (j - 1) & 1;
+          ptx::mbar_wait(&o_done[t * 2 + pb_], (scnt[pb_] - 1) & 1);
           ptx::tc_fence_after();
           const float alpha = need ? ptx::ex2(m_ref - mx2) : 1.f;
 #pragma unroll 1
@@ -333,8 +352,12 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&p_full[t * 2 + buf]);
       }
-      // ---- epilogue: PV of the unit's last block done
-      ptx::mbar_wait(&o_done[t], (sb - 1) & 1);
+      // ---- epilogue: PV of the unit's last block done (MMAs complete in issue order, so
+      // this also certifies every earlier PV of the unit)
+      {
+        const int lb = (nb - 1) & 1;
+        ptx::mbar_wait(&o_done[t * 2 + lb], (scnt[lb] - 1) & 1);
+      }
       ptx::tc_fence_after();
       const float m_use = m_ref == -INFINITY ? 0.f : m_ref;
       const float inv = l > 0.f ? 1.f / l : 0.f;

@@ -74,29 +74,47 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
       ptx::tma_prefetch_desc(&tmv32);
       ptx::tma_prefetch_desc(&tmk16);
       ptx::tma_prefetch_desc(&tmv16);
-      int unit[SW_WARPS], e[SW_WARPS], half[SW_WARPS];
+      // Per-ring state lives in registers and the metadata of the next entry / next unit
+      // is prefetched, so issuing a stage never waits on a dependent global load.
+      int unit[SW_WARPS], e[SW_WARPS], eend[SW_WARPS], kvh[SW_WARPS], half[SW_WARPS];
+      int4 cur[SW_WARPS], nxt[SW_WARPS], nu[SW_WARPS];   // KvEntry; next unit {eb, ee, kvh, -}
       uint32_t it[SW_WARPS];
+      const int4* ents = reinterpret_cast<const int4*>(p.entries);
+      auto load_unit = [&](int ui) -> int4 {
+        if (ui >= p.n_units) return make_int4(0, 0, 0, -1);
+        const Unit un = p.units[ui];
+        return make_int4(un.entry_begin, un.entry_end, un.kvh, 0);
+      };
       int active = 0;
+#pragma unroll
       for (int w = 0; w < SW_WARPS; ++w) {
         unit[w] = blockIdx.x * SW_WARPS + w;
         it[w] = 0;
         half[w] = 0;
-        e[w] = unit[w] < p.n_units ? p.units[unit[w]].entry_begin : 0;
-        active += unit[w] < p.n_units;
+        const int4 u0 = load_unit(unit[w]);
+        e[w] = u0.x;
+        eend[w] = u0.y;
+        kvh[w] = u0.z;
+        if (unit[w] < p.n_units) {
+          ++active;
+          cur[w] = ents[e[w]];
+          nxt[w] = e[w] + 1 < eend[w] ? ents[e[w] + 1] : make_int4(0, 0, 0, 0);
+        }
+        nu[w] = load_unit(unit[w] + wstride);
       }
       uint64_t idle_since = 0;
       while (active > 0) {
         bool progress = false;
+#pragma unroll
         for (int w = 0; w < SW_WARPS; ++w) {
           if (unit[w] >= p.n_units) continue;
           const uint32_t s = it[w] % SW_STAGES, ph = (it[w] / SW_STAGES) & 1;
           if (!ptx::mbar_test_wait(&empty[w * SW_STAGES + s], ph ^ 1)) continue;
           progress = true;
-          const Unit u = p.units[unit[w]];
-          const KvEntry en = p.entries[e[w]];
-          const int left = en.count - half[w] * SW_KEYS;
+          const int count = cur[w].w;
+          const int left = count - half[w] * SW_KEYS;
           const int rows = ((left < SW_KEYS ? left : SW_KEYS) + 15) & ~15;
-          const int32_t y = (en.page * p.hkv + u.kvh) * p.ps + en.row_off + half[w] * SW_KEYS;
+          const int32_t y = (cur[w].x * p.hkv + kvh[w]) * p.ps + cur[w].y + half[w] * SW_KEYS;
           uint8_t* st = smem + L.ring0 + w * L.ring_stride + s * L.stage_stride;
           uint64_t* fb = &full[w * SW_STAGES + s];
           ptx::mbar_arrive_expect_tx(fb, 2u * CH * rows * 128u);
@@ -111,12 +129,23 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
             }
           }
           ++it[w];
-          if (++half[w] * SW_KEYS >= en.count) {
+          if (++half[w] * SW_KEYS >= count) {
             half[w] = 0;
-            if (++e[w] >= u.entry_end) {
+            if (++e[w] < eend[w]) {
+              cur[w] = nxt[w];
+              if (e[w] + 1 < eend[w]) nxt[w] = ents[e[w] + 1];
+            } else {
               unit[w] += wstride;
-              if (unit[w] < p.n_units) e[w] = p.units[unit[w]].entry_begin;
-              else --active;
+              if (unit[w] < p.n_units) {
+                e[w] = nu[w].x;
+                eend[w] = nu[w].y;
+                kvh[w] = nu[w].z;
+                cur[w] = ents[e[w]];
+                nxt[w] = e[w] + 1 < eend[w] ? ents[e[w] + 1] : make_int4(0, 0, 0, 0);
+                nu[w] = load_unit(unit[w] + wstride);
+              } else {
+                --active;
+              }
             }
           }
         }

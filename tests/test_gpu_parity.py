@@ -37,9 +37,24 @@ def _cmp(w, db, requests=None, tol=None):
         assert np.max(np.abs(l - L)) <= ltol, (r, float(np.max(np.abs(l - L))))
         num += float(np.sum((o - O) ** 2))
         den += float(np.sum(O ** 2))
-    assert worst <= atol, worst
-    assert np.sqrt(num / max(den, 1e-300)) <= rtol, np.sqrt(num / den)
+    rel = np.sqrt(num / max(den, 1e-300))
+    assert worst <= atol and rel <= rtol, f"max abs {worst:.3e} (atol {atol}), rel {rel:.3e} (rtol {rtol}), {_where(w, db, ref)}"
+
     return worst
+
+
+def _where(w, db, ref):
+    """Locate the worst rows (request, query, head) to make a failure diagnosable."""
+    out = db.out.float().cpu().numpy()
+    qo = np.concatenate([[0], np.cumsum(w.q_len)])
+    worst = []
+    for r, (O, L) in ref.items():
+        err = np.abs(out[qo[r]:qo[r + 1]] - O).max(axis=-1)        # [q, Hq]
+        t, h = np.unravel_index(np.argmax(err), err.shape)
+        worst.append((float(err[t, h]), r, int(t), int(h)))
+    worst.sort(reverse=True)
+    bad_heads = sorted({h for e, _, _, h in worst if e > 1e-2})
+    return f"worst (err, req, t, head) = {worst[:4]}, heads over 1e-2: {bad_heads[:16]}"
 
 
 @pytest.fixture(scope="module", autouse=True)
