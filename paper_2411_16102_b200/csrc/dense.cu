@@ -182,64 +182,70 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       if (lane == 0) ptx::mbar_arrive(q_full);
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer =====================
+    // ===================== MMA issuer (whole warp; one elected lane issues) =====================
     // Per unit: QK(0), QK(1) for every tile, then for j = 0..nb-1 and each tile:
-    //   wait P_t(j) -> PV_t(j) (P from TMEM) -> commit o_done_t -> QK_t(j+2) into the
-    //   S buffer PV_t(j) just consumed (MMAs execute in issue order) -> commit s_full.
-    if (lane == 0) {
+    //   wait P_t(j) -> PV_t(j) (P from TMEM) -> commit o_done -> QK_t(j+2) into the S
+    //   buffer PV_t(j) just consumed (MMAs execute in issue order) -> commit s_full.
+    // The warp runs all lanes so descriptors stay warp-uniform; descriptors are built
+    // once per stage and advanced by adding (byte offset >> 4) to the start-address field.
+    {
       constexpr uint32_t IDESC_QK = ptx::umma_idesc_bf16(128, DN_KB, 0, 0);
       constexpr uint32_t IDESC_PV = ptx::umma_idesc_bf16(128, D, 0, 1);
-      const uint32_t q_addr0 = ptx::smem_u32(smem + L.q0), q_addr1 = ptx::smem_u32(smem + L.q1);
+      // descriptor halves: hi = SBO | version | swizzle (constant per operand kind),
+      // lo = start address >> 4 | LBO >> 4 << 16, advanced by immediates
+      const uint64_t qd0 = ptx::umma_desc_sw128(ptx::smem_u32(smem + L.q0), 16, 1024);
+      const uint32_t q_lo0 = (uint32_t)qd0, q_hi = (uint32_t)(qd0 >> 32);
+      const uint32_t q_lo1 = (uint32_t)ptx::umma_desc_sw128(ptx::smem_u32(smem + L.q1), 16, 1024);
+      const uint64_t kd0 = ptx::umma_desc_sw128(ptx::smem_u32(smem + L.stage0), 16, 1024);
+      const uint32_t k_lo0 = (uint32_t)kd0, k_hi = (uint32_t)(kd0 >> 32);
+      const uint64_t vd0 = ptx::umma_desc_sw128(ptx::smem_u32(smem + L.stage0 + CH * DN_KCHUNK), DN_KCHUNK, 1024);
+      const uint32_t v_lo0 = (uint32_t)vd0, v_hi = (uint32_t)(vd0 >> 32);
+      const uint32_t stage_lo = L.stage_stride >> 4;
+      const uint32_t leader = ptx::elect_one();
       uint32_t kit = 0, gu = 0;
       uint32_t pb[4] = {0, 0, 0, 0};    // completions consumed per p_full[tile][buffer]
       for (int ui = blockIdx.x; ui < p.n_units; ui += gridDim.x) {
         const Unit u = p.units[ui];
         const int nb = (u.entry_end - u.entry_begin + EPB - 1) / EPB;
         const int ntile = u.n_rows > 128 ? 2 : 1;
-        auto stage_addr = [&](int j) { return ptx::smem_u32(smem + L.stage0 + ((kit + j) % NS) * L.stage_stride); };
         auto wait_kv = [&](int j) {
           ptx::mbar_wait(&kv_full[(kit + j) % NS], ((kit + j) / NS) & 1);
           ptx::tc_fence_after();
         };
-        auto issue_qk = [&](int t, int j, uint32_t kst) {
-          const uint32_t qa = t ? q_addr1 : q_addr0;
+        auto issue_qk = [&](int t, int j) {
+          const uint32_t qlo = t ? q_lo1 : q_lo0;
+          const uint32_t klo = k_lo0 + ((kit + j) % NS) * stage_lo;
+          const uint32_t dcol = tmem + t * 128 + (j & 1) * DN_KB;
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk)
-            ptx::umma_f16(tmem + t * 128 + (j & 1) * DN_KB,
-                          ptx::umma_desc_sw128(qa + (kk / 4) * DN_QCHUNK + (kk % 4) * 32, 16, 1024),
-                          ptx::umma_desc_sw128(kst + (kk / 4) * DN_KCHUNK + (kk % 4) * 32, 16, 1024), IDESC_QK,
-                          kk > 0);
-          ptx::umma_commit(&s_full[t * 2 + (j & 1)]);
+            ptx::umma_ss_lohi(leader, dcol, qlo + (((kk / 4) * DN_QCHUNK + (kk % 4) * 32) >> 4), q_hi,
+                              klo + (((kk / 4) * DN_KCHUNK + (kk % 4) * 32) >> 4), k_hi, IDESC_QK, kk > 0);
+          ptx::umma_commit_if(leader, &s_full[t * 2 + (j & 1)]);
         };
         ptx::mbar_wait(q_full, gu & 1);
         ptx::tc_fence_after();
         for (int j = 0; j < 2 && j < nb; ++j) {
           wait_kv(j);
-          const uint32_t kst = stage_addr(j);
-          for (int t = 0; t < ntile; ++t) issue_qk(t, j, kst);
+          for (int t = 0; t < ntile; ++t) issue_qk(t, j);
         }
-        if (nb <= 2) ptx::umma_commit(q_empty);   // every QK of the unit issued: Q may be reloaded
+        if (nb <= 2) ptx::umma_commit_if(leader, q_empty);   // every QK of the unit issued: Q may be reloaded
         for (int j = 0; j < nb; ++j) {
-          const uint32_t vst = stage_addr(j) + CH * DN_KCHUNK;
-          uint32_t kst2 = 0;
-          if (j + 2 < nb) {
-            wait_kv(j + 2);
-            kst2 = stage_addr(j + 2);
-          }
+          const uint32_t vlo = v_lo0 + ((kit + j) % NS) * stage_lo;
+          if (j + 2 < nb) wait_kv(j + 2);
           for (int t = 0; t < ntile; ++t) {
             const int pi = t * 2 + (j & 1);
             ptx::mbar_wait(&p_full[pi], (pb[pi]++) & 1);
             ptx::tc_fence_after();
+            const uint32_t acol = tmem + t * 128 + (j & 1) * DN_KB;
 #pragma unroll
             for (int kk = 0; kk < DN_KB / 16; ++kk)
-              ptx::umma_f16_ts(tmem + 256 + t * D, tmem + t * 128 + (j & 1) * DN_KB + kk * 8,
-                               ptx::umma_desc_sw128(vst + kk * 16 * 128, DN_KCHUNK, 1024), IDESC_PV,
-                               (j > 0 || kk > 0) ? 1u : 0u);
-            ptx::umma_commit(&o_done[pi]);
-            if (j + 2 < nb) issue_qk(t, j + 2, kst2);
+              ptx::umma_ts_lohi(leader, tmem + 256 + t * D, acol + kk * 8, vlo + ((kk * 16 * 128) >> 4), v_hi,
+                                IDESC_PV, (j > 0 || kk > 0) ? 1u : 0u);
+            ptx::umma_commit_if(leader, &o_done[pi]);
+            if (j + 2 < nb) issue_qk(t, j + 2);
           }
-          if (j + 3 == nb) ptx::umma_commit(q_empty);   // QK(nb-1) of every tile issued
-          ptx::umma_commit(&kv_empty[(kit + j) % NS]);
+          if (j + 3 == nb) ptx::umma_commit_if(leader, q_empty);   // QK(nb-1) of every tile issued
+          ptx::umma_commit_if(leader, &kv_empty[(kit + j) % NS]);
         }
         kit += nb;
         ++gu;
