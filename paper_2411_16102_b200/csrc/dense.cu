@@ -334,24 +334,36 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
           m_ref = mx2;
         }
         const float m_use = m_ref == -INFINITY ? 0.f : m_ref;
-        float ls[4] = {0.f, 0.f, 0.f, 0.f};
-        // P = exp2(s*scale - m): 3 of every 4 on the MUFU pipe, 1 of 4 as a polynomial on
-        // the FMA pipe; bf16 pairs -> the first 32 TMEM columns of this S buffer
+        // P = exp2(s*scale - m) on packed fp32 pairs (FFMA2/FADD2): 3 of every 4 pairs on the
+        // MUFU pipe, 1 of 4 as a polynomial on the FMA pipe; bf16 pairs -> the first 32 TMEM
+        // columns of this S buffer
+        const uint64_t sc2 = ptx::f2pack(p.scale_log2, p.scale_log2), nm2 = ptx::f2pack(-m_use, -m_use);
+        uint64_t ls2[2] = {ptx::f2pack(0.f, 0.f), ptx::f2pack(0.f, 0.f)};
 #pragma unroll
         for (int c = 0; c < DN_KB / 32; ++c) {
           uint32_t pk[16];
 #pragma unroll
           for (int k = 0; k < 16; ++k) {
             const int key = c * 32 + 2 * k;
-            const float x0 = fmaf(sv[key], p.scale_log2, -m_use);
-            const float x1 = fmaf(sv[key + 1], p.scale_log2, -m_use);
-            const float p0 = ptx::ex2(x0);
-            const float p1 = (k & 1) ? ptx::exp2_poly(x1) : ptx::ex2(x1);
-            ls[k & 3] += p0 + p1;
+            const uint64_t x2 = ptx::ffma2(ptx::f2pack(sv[key], sv[key + 1]), sc2, nm2);
+            uint64_t p2;
+            if ((k & 3) == 3) {
+              p2 = ptx::exp2_poly2(x2);
+            } else {
+              float x0, x1;
+              ptx::f2unpack(x2, x0, x1);
+              p2 = ptx::f2pack(ptx::ex2(x0), ptx::ex2(x1));
+            }
+            ls2[k & 1] = ptx::fadd2(ls2[k & 1], p2);
+            float p0, p1;
+            ptx::f2unpack(p2, p0, p1);
             pk[k] = ptx::pack_bf16(p0, p1);
           }
           ptx::tmem_st16(tmem + lane_base + col_s + c * 16, pk);
         }
+        float ls[4];
+        ptx::f2unpack(ls2[0], ls[0], ls[1]);
+        ptx::f2unpack(ls2[1], ls[2], ls[3]);
         l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
         ptx::tmem_wait_st();
         ptx::tc_fence_before();

@@ -345,3 +345,45 @@ __device__ __forceinline__ void umma_commit_if(uint32_t leader, uint64_t* bar) {
 }
 }  // namespace ptx
 }  // namespace blend
+
+namespace blend {
+namespace ptx {
+// packed fp32 pairs (sm_100 FFMA2 / FADD2): two lanes of work per issue slot
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// 2^x for a pair on the FMA/ALU pipes: 2^floor(x) * p(frac), degree-3 minimax p
+// (max rel. error ~9e-5); x is clamped at -127 (result ~1e-38, i.e. 0 for softmax).
+__device__ __forceinline__ uint64_t exp2_poly2(uint64_t x2) {
+  float a, b;
+  f2unpack(x2, a, b);
+  a = fmaxf(a, -127.f);
+  b = fmaxf(b, -127.f);
+  const float fa = floorf(a), fb = floorf(b);
+  const uint64_t f = fadd2(f2pack(a, b), f2pack(-fa, -fb));
+  uint64_t p = ffma2(f, f2pack(0.0790f, 0.0790f), f2pack(0.2243f, 0.2243f));
+  p = ffma2(p, f, f2pack(0.6967f, 0.6967f));
+  p = ffma2(p, f, f2pack(1.0f, 1.0f));
+  float pa, pb;
+  f2unpack(p, pa, pb);
+  pa = __int_as_float(__float_as_int(pa) + ((int)fa << 23));
+  pb = __int_as_float(__float_as_int(pb) + ((int)fb << 23));
+  return f2pack(pa, pb);
+}
+}  // namespace ptx
+}  // namespace blend
