@@ -122,8 +122,10 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
 #pragma unroll
         for (int i = 0; i < EPB; ++i) {
           int e = un.entry_begin + j * EPB + i;
-          if (e >= un.entry_end) e = un.entry_begin;   // pad the last block (masked)
+          const bool pad = e >= un.entry_end;
+          if (pad) e = un.entry_begin;                 // pad the last block (masked: count 0)
           cur[i] = ents[e];
+          if (pad) cur[i].w = 0;
         }
       };
       if (ui < p.n_units) load_block(u, 0);
@@ -136,7 +138,10 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
           ptx::mbar_wait(&kv_empty[s], ph ^ 1);
           uint8_t* kst = smem + L.stage0 + s * L.stage_stride;
           uint8_t* vst = kst + CH * DN_KCHUNK;
-          ptx::mbar_arrive_expect_tx(&kv_full[s], 2u * CH * DN_KCHUNK);
+          int2* meta = reinterpret_cast<int2*>(smem + L.bar + 256) + s * 4;   // {pos0, count} for the softmax
+#pragma unroll
+          for (int i = 0; i < EPB; ++i) meta[i] = make_int2(cur[i].z, cur[i].w);
+          ptx::mbar_arrive_expect_tx(&kv_full[s], 2u * CH * DN_KCHUNK);   // release: meta visible to waiters
 #pragma unroll
           for (int i = 0; i < EPB; ++i) {
             const int32_t y = (cur[i].x * p.hkv + u.kvh) * p.ps + cur[i].y;   // {page, row_off, pos0, count}
@@ -261,10 +266,14 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
     const uint32_t col_o = 256 + t * D;
     uint32_t sb = 0;                                  // blocks of this tile processed so far
     uint32_t scnt[2] = {0, 0};                        // s_full completions consumed per S buffer
+    uint32_t kit_s = 0;                               // K/V stage sequence (all blocks of all units)
     for (int ui = blockIdx.x; ui < p.n_units; ui += gridDim.x) {
       const Unit u = p.units[ui];
       const int nb = (u.entry_end - u.entry_begin + EPB - 1) / EPB;
-      if (t == 1 && u.n_rows <= 128) continue;       // tile B idle for this unit
+      if (t == 1 && u.n_rows <= 128) {               // tile B idle for this unit
+        kit_s += nb;
+        continue;
+      }
       const int row = 128 * t + r;                    // row within the unit
       int32_t pos = INT32_MIN, token = 0, head = 0, tgt = PM_SKIP;
       if (row < u.n_rows) {
@@ -278,17 +287,18 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       for (int j = 0; j < nb; ++j, ++sb) {
         const int buf = j & 1;
         const uint32_t col_s = t * 128 + buf * DN_KB;
+        // key positions of this block from the stage metadata the producer wrote (the
+        // stage cannot be refilled before this block's P is consumed)
+        const uint32_t kst_idx = kit_s + j;
+        ptx::mbar_wait(&kv_full[kst_idx % NS], (kst_idx / NS) & 1);
+        const int2* meta = reinterpret_cast<const int2*>(smem + L.bar + 256) + (kst_idx % NS) * 4;
         int vis[EPB];
         bool full_vis = true;
 #pragma unroll
         for (int i = 0; i < EPB; ++i) {
-          const int e = u.entry_begin + j * EPB + i;
-          int v = 0;
-          if (e < u.entry_end) {
-            const KvEntry en = p.entries[e];
-            const int a = pos < en.pos0 ? 0 : pos - en.pos0 + 1;   // pos = INT32_MIN for padding rows
-            v = a > en.count ? en.count : a;
-          }
+          const int2 en = meta[i];                               // {pos0, count}
+          const int a = pos < en.x ? 0 : pos - en.x + 1;          // pos = INT32_MIN for padding rows
+          const int v = a > en.y ? en.y : a;
           vis[i] = v;
           full_vis = full_vis && (v == BOX);
         }
@@ -408,6 +418,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       if (tgt == PM_DIRECT) p.lse[(int64_t)token * p.hq + head] = lse2 * kLn2;
       else if (tgt >= 0) p.ws_lse[(int64_t)tgt * p.hq + head] = lse2;
       ptx::tc_fence_before();
+      kit_s += nb;
     }
   }
   __syncwarp();       // lane 0 of the producer / MMA warps rejoins its warp before the CTA barrier

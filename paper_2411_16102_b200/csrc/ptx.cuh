@@ -387,3 +387,15 @@ __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x2) {
 }
 }  // namespace ptx
 }  // namespace blend
+
+namespace blend {
+namespace ptx {
+// 16-byte cp.async with zero fill when !valid (src not read)
+__device__ __forceinline__ void cp_async16_zfill(uint32_t dst_smem, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst_smem), "l"(src), "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_group0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+}  // namespace ptx
+}  // namespace blend

@@ -35,8 +35,8 @@ __host__ __device__ inline StreamWSmem streamw_layout(int D) {
   L.stage_stride = 2 * CH * SW_CHUNK;                  // K chunks then V chunks
   L.ring_stride = SW_STAGES * L.stage_stride;
   L.ring0 = 0;
-  L.q0 = SW_WARPS * L.ring_stride;                     // per warp: CH x (16 rows x 128 B)
-  L.q_stride = CH * 2048;
+  L.q0 = SW_WARPS * L.ring_stride;                     // per warp: 2 x CH x (16 rows x 128 B)
+  L.q_stride = 2 * CH * 2048;
   L.bar = L.q0 + SW_WARPS * L.q_stride;
   L.total = L.bar + 2 * SW_WARPS * SW_STAGES * 8;
   return L;
@@ -163,30 +163,61 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
   }
 
   // ===================== consumer warp: whole units =====================
+  // The next unit's Q rows (cp.async into the other half of a double buffer) and row
+  // metadata are fetched while the current unit streams, so a unit starts without a
+  // dependent global-load round trip.
   const int g8 = lane >> 2, c4 = lane & 3;
   uint8_t* ring = smem + L.ring0 + warp * L.ring_stride;
-  uint8_t* qs = smem + L.q0 + warp * L.q_stride;
-  const uint32_t qs_u32 = ptx::smem_u32(qs);
+  const uint32_t qs_u32 = ptx::smem_u32(smem + L.q0 + warp * L.q_stride);
   uint64_t* wfull = full + warp * SW_STAGES;
   uint64_t* wempty = empty + warp * SW_STAGES;
   uint32_t it = 0;
+  constexpr int CPL = (16 * D / 8) / 32;   // 16-byte Q chunks per lane (row = lane / 2)
 
-  for (int ui = blockIdx.x * SW_WARPS + warp; ui < p.n_units; ui += wstride) {
-    const Unit u = p.units[ui];
-    // ---- Q tile (16 rows, zero padded), 128B swizzled, then A fragments
-    __syncwarp();
-#pragma unroll
-    for (int k = 0; k < (16 * D / 8) / 32; ++k) {
-      const int idx = lane + 32 * k;
-      const int r = idx / (D / 8), unit16 = idx % (D / 8);
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (r < u.n_rows) {
-        const RowInfo ri = row_info(p, u, r);
-        v = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(p.q) +
-                                                 ((int64_t)ri.token * p.hq + ri.head) * D) + unit16);
-      }
-      *reinterpret_cast<uint4*>(qs + (unit16 / 8) * 2048 + ptx::sw128(r, unit16 % 8)) = v;
+  struct RowMeta {
+    RowInfo r0, r1;
+    int32_t pos0, pos1;
+  };
+  auto fetch_q = [&](const Unit& un, int buf) {
+    const int r = lane >> 1;
+    const bool valid = r < un.n_rows;
+    const __nv_bfloat16* src = reinterpret_cast<const __nv_bfloat16*>(p.q);
+    if (valid) {
+      const RowInfo ri = row_info(p, un, r);
+      src += ((int64_t)ri.token * p.hq + ri.head) * D;
     }
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) {
+      const int unit16 = (lane & 1) * CPL + k;
+      ptx::cp_async16_zfill(qs_u32 + buf * (CH * 2048) + (unit16 / 8) * 2048 + ptx::sw128(r, unit16 % 8),
+                            src + 8 * unit16, valid);
+    }
+    ptx::cp_async_commit();
+  };
+  auto fetch_meta = [&](const Unit& un) {
+    RowMeta m{{0, 0, 0}, {0, 0, 0}, INT32_MIN, INT32_MIN};
+    if (g8 < un.n_rows) {
+      m.r0 = row_info(p, un, g8);
+      m.pos0 = p.tok_pos[m.r0.token];
+    }
+    if (g8 + 8 < un.n_rows) {
+      m.r1 = row_info(p, un, g8 + 8);
+      m.pos1 = p.tok_pos[m.r1.token];
+    }
+    return m;
+  };
+
+  int ui = blockIdx.x * SW_WARPS + warp;
+  Unit u_next = ui < p.n_units ? p.units[ui] : Unit{};
+  RowMeta meta_next{};
+  if (ui < p.n_units) {
+    fetch_q(u_next, 0);
+    meta_next = fetch_meta(u_next);
+  }
+  for (int buf = 0; ui < p.n_units; ui += wstride, buf ^= 1) {
+    const Unit u = u_next;
+    const RowMeta meta = meta_next;
+    ptx::cp_async_wait_group0();
     __syncwarp();
     uint32_t qa[D / 16][4];
 #pragma unroll
@@ -194,19 +225,17 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
       const int mi = lane >> 3;
       const int row = (mi & 1) * 8 + (lane & 7);
       const int unit16 = 2 * kk + (mi >> 1);
-      ptx::ldsm_x4(qs_u32 + (unit16 / 8) * 2048 + ptx::sw128(row, unit16 % 8), qa[kk][0], qa[kk][1], qa[kk][2],
-                   qa[kk][3]);
+      ptx::ldsm_x4(qs_u32 + buf * (CH * 2048) + (unit16 / 8) * 2048 + ptx::sw128(row, unit16 % 8), qa[kk][0],
+                   qa[kk][1], qa[kk][2], qa[kk][3]);
     }
-    int32_t pos0r = INT32_MIN, pos1r = INT32_MIN;
-    RowInfo ri0{0, 0, 0}, ri1{0, 0, 0};
-    if (g8 < u.n_rows) {
-      ri0 = row_info(p, u, g8);
-      pos0r = p.tok_pos[ri0.token];
+    __syncwarp();   // every lane's ldmatrix of this buffer is done before the next prefetch targets it later
+    if (ui + wstride < p.n_units) {
+      u_next = p.units[ui + wstride];
+      fetch_q(u_next, buf ^ 1);
+      meta_next = fetch_meta(u_next);
     }
-    if (g8 + 8 < u.n_rows) {
-      ri1 = row_info(p, u, g8 + 8);
-      pos1r = p.tok_pos[ri1.token];
-    }
+    const RowInfo ri0 = meta.r0, ri1 = meta.r1;
+    const int32_t pos0r = meta.pos0, pos1r = meta.pos1;
 
     float o[NT][4];
 #pragma unroll
