@@ -138,10 +138,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
           ptx::mbar_wait(&kv_empty[s], ph ^ 1);
           uint8_t* kst = smem + L.stage0 + s * L.stage_stride;
           uint8_t* vst = kst + CH * DN_KCHUNK;
-          int2* meta = reinterpret_cast<int2*>(smem + L.bar + 256) + s * 4;   // {pos0, count} for the softmax
-#pragma unroll
-          for (int i = 0; i < EPB; ++i) meta[i] = make_int2(cur[i].z, cur[i].w);
-          ptx::mbar_arrive_expect_tx(&kv_full[s], 2u * CH * DN_KCHUNK);   // release: meta visible to waiters
+          ptx::mbar_arrive_expect_tx(&kv_full[s], 2u * CH * DN_KCHUNK);
 #pragma unroll
           for (int i = 0; i < EPB; ++i) {
             const int32_t y = (cur[i].x * p.hkv + u.kvh) * p.ps + cur[i].y;   // {page, row_off, pos0, count}
@@ -266,14 +263,18 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
     const uint32_t col_o = 256 + t * D;
     uint32_t sb = 0;                                  // blocks of this tile processed so far
     uint32_t scnt[2] = {0, 0};                        // s_full completions consumed per S buffer
-    uint32_t kit_s = 0;                               // K/V stage sequence (all blocks of all units)
+    int2 enext[EPB];                                  // {pos0, count} of the next block's entries
+    auto load_meta = [&](const Unit& un, int j) {
+#pragma unroll
+      for (int i = 0; i < EPB; ++i) {
+        const int e = un.entry_begin + j * EPB + i;
+        enext[i] = e < un.entry_end ? make_int2(p.entries[e].pos0, p.entries[e].count) : make_int2(0, 0);
+      }
+    };
     for (int ui = blockIdx.x; ui < p.n_units; ui += gridDim.x) {
       const Unit u = p.units[ui];
       const int nb = (u.entry_end - u.entry_begin + EPB - 1) / EPB;
-      if (t == 1 && u.n_rows <= 128) {               // tile B idle for this unit
-        kit_s += nb;
-        continue;
-      }
+      if (t == 1 && u.n_rows <= 128) continue;       // tile B idle for this unit
       const int row = 128 * t + r;                    // row within the unit
       int32_t pos = INT32_MIN, token = 0, head = 0, tgt = PM_SKIP;
       if (row < u.n_rows) {
@@ -284,19 +285,22 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         tgt = row_target(p, u, ri.tl);
       }
       float m_ref = -INFINITY, l = 0.f;
+      load_meta(u, 0);
       for (int j = 0; j < nb; ++j, ++sb) {
         const int buf = j & 1;
         const uint32_t col_s = t * 128 + buf * DN_KB;
         // key positions of this block from the stage metadata the producer wrote (the
         // stage cannot be refilled before this block's P is consumed)
-        const uint32_t kst_idx = kit_s + j;
-        ptx::mbar_wait(&kv_full[kst_idx % NS], (kst_idx / NS) & 1);
-        const int2* meta = reinterpret_cast<const int2*>(smem + L.bar + 256) + (kst_idx % NS) * 4;
+        // this block's {pos0, count} were loaded one block ahead (latency off the critical path)
+        int2 ecur[EPB];
+#pragma unroll
+        for (int i = 0; i < EPB; ++i) ecur[i] = enext[i];
+        if (j + 1 < nb) load_meta(u, j + 1);
         int vis[EPB];
         bool full_vis = true;
 #pragma unroll
         for (int i = 0; i < EPB; ++i) {
-          const int2 en = meta[i];                               // {pos0, count}
+          const int2 en = ecur[i];                               // {pos0, count}
           const int a = pos < en.x ? 0 : pos - en.x + 1;          // pos = INT32_MIN for padding rows
           const int v = a > en.y ? en.y : a;
           vis[i] = v;
@@ -418,7 +422,6 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       if (tgt == PM_DIRECT) p.lse[(int64_t)token * p.hq + head] = lse2 * kLn2;
       else if (tgt >= 0) p.ws_lse[(int64_t)tgt * p.hq + head] = lse2;
       ptx::tc_fence_before();
-      kit_s += nb;
     }
   }
   __syncwarp();       // lane 0 of the producer / MMA warps rejoins its warp before the CTA barrier
