@@ -198,7 +198,9 @@ typedef struct {
   int64_t n_cache_pages;     /* pages in the cache allocations (page ids must be < this)     */
   void* out;                 /* device [sum q, Hq, D] (kv dtype), written                    */
   float* lse;                /* device [sum q, Hq] fp32 natural-log LSE, written             */
-  void* workspace;           /* device, >= blend_workspace_bytes, contents scratch           */
+  void* workspace;           /* device, >= blend_workspace_bytes (always required), contents
+                                scratch: partial (o, lse) rows + the streaming pass's unit
+                                counter; one call in flight per workspace                    */
   size_t workspace_bytes;
   const blend_plan* plan;    /* from blend_plan_upload (its buffer must be resident)         */
   int32_t path;              /* BLEND_PATH_*: AUTO = tcgen05 dense + streaming (+ generic for

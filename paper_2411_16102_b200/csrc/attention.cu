@@ -80,8 +80,9 @@ extern "C" int blend_attention(const blend_attn_args* a, void* stream) {
   const int64_t prow = pl.count[SEC_COUNT];
   const int hq = pl.num_q_heads, D = pl.head_dim;
   size_t o_bytes = ((size_t)prow * hq * D * 4 + 255) & ~size_t(255);
-  size_t need = o_bytes + (((size_t)prow * hq * 4 + 255) & ~size_t(255));
-  if (prow > 0 && (!a->workspace || a->workspace_bytes < need))
+  const size_t lse_bytes = ((size_t)prow * hq * 4 + 255) & ~size_t(255);
+  const size_t need = o_bytes + lse_bytes + 256;   // + the streaming pass's unit counter
+  if (!a->workspace || a->workspace_bytes < need)
     return blend_internal_fail(BLEND_ENOSPC, "attention: workspace too small");
   if (a->n_cache_pages <= 0) return blend_internal_fail(BLEND_EINVAL, "attention: n_cache_pages");
 
@@ -94,6 +95,7 @@ extern "C" int blend_attention(const blend_attn_args* a, void* stream) {
   p.lse = a->lse;
   p.ws_o = (float*)a->workspace;
   p.ws_lse = (float*)((char*)a->workspace + o_bytes);
+  p.sched = (int32_t*)((char*)a->workspace + o_bytes + lse_bytes);
   p.tok_pos = (const int32_t*)(base + pl.off[SEC_TOK_POS]);
   p.item_tokens = (const int32_t*)(base + pl.off[SEC_ITEM_TOKENS]);
   p.entries = (const KvEntry*)(base + pl.off[SEC_ENTRIES]);
@@ -101,6 +103,7 @@ extern "C" int blend_attention(const blend_attn_args* a, void* stream) {
   p.merge_tok = (const int32_t*)(base + pl.off[SEC_MERGE_TOK]);
   p.merge_off = (const int32_t*)(base + pl.off[SEC_MERGE_OFF]);
   p.merge_rows = (const int32_t*)(base + pl.off[SEC_MERGE_ROWS]);
+  p.srows = (const RowDesc*)(base + pl.off[SEC_STREAM_ROWS]);
   p.n_merge = (int32_t)pl.count[SEC_MERGE_TOK];
   p.hq = hq;
   p.hkv = pl.num_kv_heads;
@@ -122,6 +125,16 @@ extern "C" int blend_attention(const blend_attn_args* a, void* stream) {
   AttnParams pd = p;
   pd.units = (const Unit*)(base + pl.off[SEC_DENSE_UNITS]);
   pd.n_units = (int32_t)pl.count[SEC_DENSE_UNITS];
+  // The streaming pass hands out units through a counter in the workspace.  The tcgen05
+  // dense kernel zeroes it before its launch trigger (so the overlapped streaming grid
+  // sees 0); without that kernel a memset ahead of the passes does.
+  const bool stream_dyn = !generic && pl.count[SEC_STREAM_UNITS] > 0 && n_merge_all == n_merge_unfused;
+  const bool dense_tc = !generic && a->path != BLEND_PATH_NO_TCGEN05 && pd.n_units > 0;
+  pd.sched = stream_dyn && dense_tc ? p.sched : nullptr;
+  if (stream_dyn && !dense_tc) {
+    e = cudaMemsetAsync(p.sched, 0, sizeof(int32_t), st);
+    if (e != cudaSuccess) return cuda_fail(e);
+  }
   if (generic || a->path == BLEND_PATH_NO_TCGEN05) e = launch_generic(pd, st);
   else e = launch_dense(pd, a->n_cache_pages, st);
   if (e != cudaSuccess) return cuda_fail(e);

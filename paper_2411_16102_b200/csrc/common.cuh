@@ -34,6 +34,8 @@ struct AttnParams {
   int32_t kv_f32;   // 1: fp32 q/k/v/out, 0: bf16
   float scale_log2; // log2(e) / sqrt(D)
   int32_t avg_entries;   // host-side launch heuristic: mean entries per unit
+  const RowDesc* srows;  // streaming units' row descriptors (SEC_STREAM_ROWS)
+  int32_t* sched;        // workspace word: dynamic unit counter of the streaming pass (zeroed per call)
 };
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {

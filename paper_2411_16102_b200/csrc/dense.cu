@@ -79,6 +79,15 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 30);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (p.sched != nullptr && blockIdx.x == 0) {
+    // reset the streaming pass's unit counter before this CTA's launch trigger: the
+    // dependent (streaming) grid cannot start before every CTA of this grid has triggered
+    if (threadIdx.x == 0) {
+      if (atomicExch(p.sched, 0) == 0x7fffffff) __trap();   // consumes the result: the exchange has completed
+      __threadfence();
+    }
+    __syncthreads();
+  }
   ptx::pdl_launch_dependents();   // the streaming pass may start on SMs this grid leaves free
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {

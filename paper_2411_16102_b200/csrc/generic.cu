@@ -158,28 +158,51 @@ __global__ void __launch_bounds__(256) merge_kernel(AttnParams p) {
   const int D = p.d;
   const int vec = D / 32;          // 2 or 4 elements per lane
   const int e0 = lane * vec;
-  float mx = -INFINITY;
-  for (int s = s0; s < s1; ++s) mx = fmaxf(mx, p.ws_lse[(int64_t)p.merge_rows[s] * p.hq + h]);
+  // One pass in chunks of MCH sources: every load of a chunk is issued before any is
+  // used (rows -> lse -> o are the only dependent steps), then an online rescale.
+  constexpr int MCH = 4;
+  float mx = -INFINITY, tot = 0.f;
   float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  float tot = 0.f;
-  if (mx != -INFINITY) {
-    for (int s = s0; s < s1; ++s) {
-      const int64_t row = p.merge_rows[s];
-      const float w = exp2f(p.ws_lse[row * p.hq + h] - mx);
-      tot += w;
-      const float* src = p.ws_o + (row * p.hq + h) * D + e0;
-      if (vec == 4) {
-        const float4 v = *reinterpret_cast<const float4*>(src);
-        acc[0] = fmaf(w, v.x, acc[0]);
-        acc[1] = fmaf(w, v.y, acc[1]);
-        acc[2] = fmaf(w, v.z, acc[2]);
-        acc[3] = fmaf(w, v.w, acc[3]);
-      } else {
-        const float2 v = *reinterpret_cast<const float2*>(src);
-        acc[0] = fmaf(w, v.x, acc[0]);
-        acc[1] = fmaf(w, v.y, acc[1]);
+  for (int c0 = s0; c0 < s1; c0 += MCH) {
+    int64_t row[MCH];
+    float l[MCH];
+    float4 v[MCH];
+#pragma unroll
+    for (int i = 0; i < MCH; ++i) row[i] = c0 + i < s1 ? (int64_t)p.merge_rows[c0 + i] : -1;
+#pragma unroll
+    for (int i = 0; i < MCH; ++i) l[i] = row[i] >= 0 ? p.ws_lse[row[i] * p.hq + h] : -INFINITY;
+#pragma unroll
+    for (int i = 0; i < MCH; ++i) {
+      v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (row[i] >= 0) {
+        const float* src = p.ws_o + (row[i] * p.hq + h) * D + e0;
+        if (vec == 4) {
+          v[i] = *reinterpret_cast<const float4*>(src);
+        } else {
+          const float2 t = *reinterpret_cast<const float2*>(src);
+          v[i].x = t.x;
+          v[i].y = t.y;
+        }
       }
     }
+    float cm = mx;
+#pragma unroll
+    for (int i = 0; i < MCH; ++i) cm = fmaxf(cm, l[i]);
+    if (cm == -INFINITY) continue;
+    const float a = exp2f(mx - cm);      // mx = -inf on the first live chunk -> 0
+    tot *= a;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc[k] *= a;
+#pragma unroll
+    for (int i = 0; i < MCH; ++i) {
+      const float w = exp2f(l[i] - cm);  // l = -inf (absent source) -> 0
+      tot += w;
+      acc[0] = fmaf(w, v[i].x, acc[0]);
+      acc[1] = fmaf(w, v[i].y, acc[1]);
+      acc[2] = fmaf(w, v[i].z, acc[2]);
+      acc[3] = fmaf(w, v[i].w, acc[3]);
+    }
+    mx = cm;
   }
   const float inv = tot > 0.f ? 1.f / tot : 0.f;
   const int64_t ob = ((int64_t)token * p.hq + h) * D + e0;

@@ -729,6 +729,27 @@ int build_plan(blend_tree* t) {
   for (size_t ii = 0; ii < items.size(); ++ii)
     std::copy(items[ii].toks.begin(), items[ii].toks.end(), item_tokens.begin() + item_tok_off[ii]);
 
+  // Per-row descriptors of the streaming units (STREAM_ROWS slots per unit): the
+  // kernel gets each row's q/out row, position and partmap target in one load
+  // instead of the item_tokens -> tok_pos / partmap chain.
+  std::vector<blend::RowDesc> srows(sunits.size() * blend::STREAM_ROWS,
+                                    blend::RowDesc{-1, INT32_MIN, blend::PM_SKIP, -1});
+  {
+    const int32_t g = a.num_q_heads / a.num_kv_heads;
+    for (size_t ui = 0; ui < sunits.size(); ++ui) {
+      const blend::Unit& u = sunits[ui];
+      for (int r = 0; r < u.n_rows; ++r) {
+        const int32_t ir = u.row_begin + r, tl = ir / g, j = ir % g;
+        const int32_t tok = item_tokens[u.tok_base + tl];
+        blend::RowDesc& d = srows[ui * blend::STREAM_ROWS + r];
+        d.qrow = tok * a.num_q_heads + u.kvh * g + j;
+        d.pos = tok_pos[tok];
+        d.target = partmap[u.pm_base + tl];
+        d.head = u.kvh * g + j;
+      }
+    }
+  }
+
   // ---- serialise sections (16-byte aligned)
   using namespace blend;
   std::vector<uint8_t>& blob = t->plan_blob;
@@ -750,13 +771,13 @@ int build_plan(blend_tree* t) {
   put(SEC_MERGE_TOK, merge_tok.data(), 4, merge_tok.size());
   put(SEC_MERGE_OFF, merge_off.data(), 4, merge_off.size());
   put(SEC_MERGE_ROWS, merge_rows.data(), 4, merge_rows.size());
+  put(SEC_STREAM_ROWS, srows.data(), sizeof(RowDesc), srows.size());
   blob.resize((blob.size() + 255) & ~size_t(255));
 
   t->n_partial_rows = prow;
   const size_t hq = a.num_q_heads, D = a.head_dim;
   size_t o_bytes = ((size_t)prow * hq * D * 4 + 255) & ~size_t(255);
-  t->workspace_bytes = o_bytes + (((size_t)prow * hq * 4 + 255) & ~size_t(255));
-  if (t->workspace_bytes == 0) t->workspace_bytes = 256;
+  t->workspace_bytes = o_bytes + (((size_t)prow * hq * 4 + 255) & ~size_t(255)) + 256;   // + unit counter
   t->info.n_tokens = T;
   t->info.n_items = (int64_t)items.size();
   t->info.n_dense_units = (int64_t)dunits.size();

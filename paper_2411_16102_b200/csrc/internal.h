@@ -17,6 +17,7 @@ enum PlanSection {
   SEC_MERGE_TOK,       // int32[M]   tokens with >= 2 sources
   SEC_MERGE_OFF,       // int32[M+1]
   SEC_MERGE_ROWS,      // int32[]    partial rows, ascending key-range start (-1 = the fusing unit)
+  SEC_STREAM_ROWS,     // RowDesc[n_stream * STREAM_ROWS]  per-row descriptors of the streaming units
   SEC_COUNT
 };
 
@@ -44,6 +45,14 @@ struct Unit {
   int32_t entry_end;
   int32_t pm_base;     // partmap index of token_local 0 for this (item, split)
   int32_t tok_base;    // item_tok_off[item]
+};
+
+// Row r of a streaming unit, precomputed by the planner (padding rows: qrow = -1).
+struct RowDesc {
+  int32_t qrow;      // token * Hq + q head: row of q / out / lse
+  int32_t pos;       // absolute position of the token (causal bound)
+  int32_t target;    // partmap value: partial row | PM_DIRECT | PM_SKIP | fused
+  int32_t head;      // q head (partial-row column)
 };
 
 constexpr int DENSE_ROWS = 256;    // rows per dense unit: two 128-row tcgen05 Q tiles (UMMA M=128)

@@ -3,12 +3,18 @@
 // Same contract as stream.cu (SMALL units: <= 16 rows of one kv head over their page
 // entries; PAPER §2.3, §7.2), organised so that a unit never needs a
 // CTA barrier: each of the 4 consumer warps owns whole units and a private 3-stage
-// ring of 32-key K/V half-entries in shared memory; one TMA producer warp serves the
-// four rings round-robin (non-blocking mbarrier.test_wait), loading only the 16-row
-// groups that hold valid slots.  A warp keeps the unit's full online-softmax state
-// (m, l, O[16 x D] in mma.sync fragments), so short decode units (~100-token private
-// suffixes) cost no cross-warp merge and no named-barrier stalls, and long units
-// (16K-token contexts) stream at HBM speed with 4 units in flight per SM.
+// ring of 32-key K/V half-entries in shared memory, fed by its own TMA producer warp
+// that loads only the 16-row groups holding valid slots.  A warp keeps the unit's full
+// online-softmax state (m, l, O[16 x D] in mma.sync fragments), so short decode units
+// (~100-token private suffixes) cost no cross-warp merge and no named-barrier stalls,
+// and long units (16K-token contexts) stream at HBM speed with 4 units in flight per SM.
+//
+// Units are handed out dynamically (one global atomic counter, reset by the launch):
+// the planner orders them longest-first, so this is greedy LPT, and CTAs that start
+// late because the overlapped dense pass still occupies their SM simply take fewer
+// units.  A ring's producer fetches unit k+1 while streaming unit k and announces it
+// to its consumer through a two-slot smem queue, so the consumer prefetches the next
+// unit's Q rows and row metadata while the current one streams.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <math.h>
@@ -19,14 +25,14 @@
 
 namespace blend {
 
-constexpr int SW_WARPS = 4;
-constexpr int SW_THREADS = 32 * (SW_WARPS + 1);
+constexpr int SW_WARPS = 4;                  // consumer warps = rings = producer warps
+constexpr int SW_THREADS = 32 * (2 * SW_WARPS);
 constexpr int SW_STAGES = 3;
 constexpr int SW_KEYS = 32;                  // keys per stage (half a 64-slot entry)
 constexpr int SW_CHUNK = SW_KEYS * 128;      // 32 rows x 128 B
 
 struct StreamWSmem {
-  uint32_t ring0, ring_stride, stage_stride, q0, q_stride, bar, total;
+  uint32_t ring0, ring_stride, stage_stride, q0, q_stride, bar, uq, total;
 };
 
 __host__ __device__ inline StreamWSmem streamw_layout(int D) {
@@ -38,7 +44,8 @@ __host__ __device__ inline StreamWSmem streamw_layout(int D) {
   L.q0 = SW_WARPS * L.ring_stride;                     // per warp: 2 x CH x (16 rows x 128 B)
   L.q_stride = 2 * CH * 2048;
   L.bar = L.q0 + SW_WARPS * L.q_stride;
-  L.total = L.bar + 2 * SW_WARPS * SW_STAGES * 8;
+  L.uq = L.bar + 2 * SW_WARPS * SW_STAGES * 8 + 2 * SW_WARPS * 2 * 8;   // + unit-queue barriers
+  L.total = L.uq + SW_WARPS * 2 * 4;
   return L;
 }
 
@@ -54,8 +61,10 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
   const StreamWSmem L = streamw_layout(D);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar);     // [warp][stage]
   uint64_t* empty = full + SW_WARPS * SW_STAGES;
+  uint64_t* uqf = empty + SW_WARPS * SW_STAGES;   // [ring][2] unit index announced
+  uint64_t* uqe = uqf + SW_WARPS * 2;             // [ring][2] announcement consumed
+  int32_t* uq = reinterpret_cast<int32_t*>(smem + L.uq);   // [ring][2] unit index (>= n_units: done)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wstride = SW_WARPS * gridDim.x;
   ptx::pdl_launch_dependents();
 
   if (threadIdx.x == 0) {
@@ -63,98 +72,84 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
       ptx::mbar_init(&full[i], 1);
       ptx::mbar_init(&empty[i], 1);
     }
+    for (int i = 0; i < SW_WARPS * 2; ++i) {
+      ptx::mbar_init(&uqf[i], 1);
+      ptx::mbar_init(&uqe[i], 1);
+    }
     ptx::fence_mbar_init();
   }
   __syncthreads();
 
-  if (warp == SW_WARPS) {
-    // ===================== TMA producer: 4 rings, round-robin =====================
+  if (warp >= SW_WARPS) {
+    // ===================== TMA producer of ring w =====================
+    const int w = warp - SW_WARPS;
     if (lane == 0) {
       ptx::tma_prefetch_desc(&tmk32);
       ptx::tma_prefetch_desc(&tmv32);
       ptx::tma_prefetch_desc(&tmk16);
       ptx::tma_prefetch_desc(&tmv16);
-      // Per-ring state lives in registers and the metadata of the next entry / next unit
-      // is prefetched, so issuing a stage never waits on a dependent global load.
-      int unit[SW_WARPS], e[SW_WARPS], eend[SW_WARPS], kvh[SW_WARPS], half[SW_WARPS];
-      int4 cur[SW_WARPS], nxt[SW_WARPS], nu[SW_WARPS];   // KvEntry; next unit {eb, ee, kvh, -}
-      uint32_t it[SW_WARPS];
       const int4* ents = reinterpret_cast<const int4*>(p.entries);
-      auto load_unit = [&](int ui) -> int4 {
-        if (ui >= p.n_units) return make_int4(0, 0, 0, -1);
-        const Unit un = p.units[ui];
-        return make_int4(un.entry_begin, un.entry_end, un.kvh, 0);
+      uint64_t* rfull = full + w * SW_STAGES;
+      uint64_t* rempty = empty + w * SW_STAGES;
+      uint8_t* ring = smem + L.ring0 + w * L.ring_stride;
+      uint32_t a = 0, it = 0;
+      auto announce = [&](int idx) {
+        const uint32_t s = a & 1, ph = (a >> 1) & 1;
+        ptx::mbar_wait(&uqe[w * 2 + s], ph ^ 1);
+        uq[w * 2 + s] = idx;
+        ptx::mbar_arrive(&uqf[w * 2 + s]);   // release: the consumer reads the slot after its wait
+        ++a;
       };
-      int active = 0;
+      int idx = atomicAdd(p.sched, 1);
+      announce(idx);
+      if (idx < p.n_units) {
+        Unit un = p.units[idx];
+        int nidx = atomicAdd(p.sched, 1);   // consumed one unit later
+        int4 cur = ents[un.entry_begin];
+        while (true) {
+          Unit nun{};
+          int4 nfirst = make_int4(0, 0, 0, 0);
+          int phase = 0;   // 1: next unit announced and its Unit requested, 2: its first entry requested
+          for (int e = un.entry_begin; e < un.entry_end; ++e) {
+            const int4 nxt = e + 1 < un.entry_end ? ents[e + 1] : make_int4(0, 0, 0, 0);
+            const int count = cur.w;
+            for (int h = 0; h * SW_KEYS < count; ++h, ++it) {
+              const uint32_t s = it % SW_STAGES, ph = (it / SW_STAGES) & 1;
+              ptx::mbar_wait(&rempty[s], ph ^ 1);
+              const int left = count - h * SW_KEYS;
+              const int rows = ((left < SW_KEYS ? left : SW_KEYS) + 15) & ~15;
+              const int32_t y = (cur.x * p.hkv + un.kvh) * p.ps + cur.y + h * SW_KEYS;
+              uint8_t* st = ring + s * L.stage_stride;
+              ptx::mbar_arrive_expect_tx(&rfull[s], 2u * CH * rows * 128u);
 #pragma unroll
-      for (int w = 0; w < SW_WARPS; ++w) {
-        unit[w] = blockIdx.x * SW_WARPS + w;
-        it[w] = 0;
-        half[w] = 0;
-        const int4 u0 = load_unit(unit[w]);
-        e[w] = u0.x;
-        eend[w] = u0.y;
-        kvh[w] = u0.z;
-        if (unit[w] < p.n_units) {
-          ++active;
-          cur[w] = ents[e[w]];
-          nxt[w] = e[w] + 1 < eend[w] ? ents[e[w] + 1] : make_int4(0, 0, 0, 0);
-        }
-        nu[w] = load_unit(unit[w] + wstride);
-      }
-      uint64_t idle_since = 0;
-      while (active > 0) {
-        bool progress = false;
-#pragma unroll
-        for (int w = 0; w < SW_WARPS; ++w) {
-          if (unit[w] >= p.n_units) continue;
-          const uint32_t s = it[w] % SW_STAGES, ph = (it[w] / SW_STAGES) & 1;
-          if (!ptx::mbar_test_wait(&empty[w * SW_STAGES + s], ph ^ 1)) continue;
-          progress = true;
-          const int count = cur[w].w;
-          const int left = count - half[w] * SW_KEYS;
-          const int rows = ((left < SW_KEYS ? left : SW_KEYS) + 15) & ~15;
-          const int32_t y = (cur[w].x * p.hkv + kvh[w]) * p.ps + cur[w].y + half[w] * SW_KEYS;
-          uint8_t* st = smem + L.ring0 + w * L.ring_stride + s * L.stage_stride;
-          uint64_t* fb = &full[w * SW_STAGES + s];
-          ptx::mbar_arrive_expect_tx(fb, 2u * CH * rows * 128u);
-#pragma unroll
-          for (int c = 0; c < CH; ++c) {
-            if (rows == SW_KEYS) {
-              ptx::tma_load_2d(st + c * SW_CHUNK, &tmk32, fb, c * 64, y);
-              ptx::tma_load_2d(st + (CH + c) * SW_CHUNK, &tmv32, fb, c * 64, y);
-            } else {
-              ptx::tma_load_2d(st + c * SW_CHUNK, &tmk16, fb, c * 64, y);
-              ptx::tma_load_2d(st + (CH + c) * SW_CHUNK, &tmv16, fb, c * 64, y);
-            }
-          }
-          ++it[w];
-          if (++half[w] * SW_KEYS >= count) {
-            half[w] = 0;
-            if (++e[w] < eend[w]) {
-              cur[w] = nxt[w];
-              if (e[w] + 1 < eend[w]) nxt[w] = ents[e[w] + 1];
-            } else {
-              unit[w] += wstride;
-              if (unit[w] < p.n_units) {
-                e[w] = nu[w].x;
-                eend[w] = nu[w].y;
-                kvh[w] = nu[w].z;
-                cur[w] = ents[e[w]];
-                nxt[w] = e[w] + 1 < eend[w] ? ents[e[w] + 1] : make_int4(0, 0, 0, 0);
-                nu[w] = load_unit(unit[w] + wstride);
-              } else {
-                --active;
+              for (int c = 0; c < CH; ++c) {
+                if (rows == SW_KEYS) {
+                  ptx::tma_load_2d(st + c * SW_CHUNK, &tmk32, &rfull[s], c * 64, y);
+                  ptx::tma_load_2d(st + (CH + c) * SW_CHUNK, &tmv32, &rfull[s], c * 64, y);
+                } else {
+                  ptx::tma_load_2d(st + c * SW_CHUNK, &tmk16, &rfull[s], c * 64, y);
+                  ptx::tma_load_2d(st + (CH + c) * SW_CHUNK, &tmv16, &rfull[s], c * 64, y);
+                }
+              }
+              // the unit's first loads are in flight: hand out the next unit, then fetch its
+              // metadata one stage later, so no dependent load sits right before a TMA issue
+              if (phase == 1 && nidx < p.n_units) {
+                nfirst = ents[nun.entry_begin];
+                phase = 2;
+              }
+              if (phase == 0) {
+                announce(nidx);
+                if (nidx < p.n_units) nun = p.units[nidx];
+                phase = 1;
               }
             }
+            cur = nxt;
           }
-        }
-        if (progress) {
-          idle_since = 0;
-        } else {   // watchdog: no ring has freed a stage for 10 s -> protocol bug, fail loudly
-          const uint64_t now = ptx::globaltimer_ns();
-          if (idle_since == 0) idle_since = now;
-          else if (now - idle_since > 10000000000ull) __trap();
+          if (nidx >= p.n_units) break;
+          if (phase == 1) nfirst = ents[nun.entry_begin];
+          un = nun;
+          cur = nfirst;
+          nidx = atomicAdd(p.sched, 1);
         }
       }
     }
@@ -163,60 +158,61 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
   }
 
   // ===================== consumer warp: whole units =====================
-  // The next unit's Q rows (cp.async into the other half of a double buffer) and row
-  // metadata are fetched while the current unit streams, so a unit starts without a
-  // dependent global-load round trip.
+  // The next unit's Q rows (cp.async into the other half of a double buffer), row
+  // descriptors and first 32 page entries (one per lane) are fetched while the current
+  // unit streams, so a unit starts without a dependent global-load round trip.
   const int g8 = lane >> 2, c4 = lane & 3;
   uint8_t* ring = smem + L.ring0 + warp * L.ring_stride;
   const uint32_t qs_u32 = ptx::smem_u32(smem + L.q0 + warp * L.q_stride);
   uint64_t* wfull = full + warp * SW_STAGES;
   uint64_t* wempty = empty + warp * SW_STAGES;
+  const int4* ents = reinterpret_cast<const int4*>(p.entries);
   uint32_t it = 0;
   constexpr int CPL = (16 * D / 8) / 32;   // 16-byte Q chunks per lane (row = lane / 2)
 
-  struct RowMeta {
-    RowInfo r0, r1;
-    int32_t pos0, pos1;
+  uint32_t a = 0;
+  auto next_index = [&]() -> int {   // the ring's next announced unit (>= n_units: no more work)
+    const uint32_t s = a & 1, ph = (a >> 1) & 1;
+    ptx::mbar_wait(&uqf[warp * 2 + s], ph);
+    const int idx = uq[warp * 2 + s];
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(&uqe[warp * 2 + s]);
+    ++a;
+    return idx;
   };
-  auto fetch_q = [&](const Unit& un, int buf) {
-    const int r = lane >> 1;
-    const bool valid = r < un.n_rows;
-    const __nv_bfloat16* src = reinterpret_cast<const __nv_bfloat16*>(p.q);
-    if (valid) {
-      const RowInfo ri = row_info(p, un, r);
-      src += ((int64_t)ri.token * p.hq + ri.head) * D;
-    }
+  struct Pre {
+    RowDesc d0, d1;        // rows g8 and g8 + 8 (softmax / output rows of this lane)
+    int eb, ne;            // entry range
+    int4 ebatch;           // entry eb + lane (lane < ne)
+  };
+  // issue every load of unit idx; Q goes to buffer buf by cp.async
+  auto prefetch = [&](int idx, int buf) -> Pre {
+    Pre r;
+    const RowDesc* rd = p.srows + (int64_t)idx * STREAM_ROWS;
+    const RowDesc dq = rd[lane >> 1];
+    r.d0 = rd[g8];
+    r.d1 = rd[g8 + 8];
+    const int2 er = *reinterpret_cast<const int2*>(&p.units[idx].entry_begin);
+    r.eb = er.x;
+    r.ne = er.y - er.x;
+    r.ebatch = lane < r.ne ? ents[r.eb + lane] : make_int4(0, 0, 0, 0);
+    const bool valid = dq.qrow >= 0;
+    const __nv_bfloat16* src = reinterpret_cast<const __nv_bfloat16*>(p.q) + (valid ? (int64_t)dq.qrow * D : 0);
 #pragma unroll
     for (int k = 0; k < CPL; ++k) {
       const int unit16 = (lane & 1) * CPL + k;
-      ptx::cp_async16_zfill(qs_u32 + buf * (CH * 2048) + (unit16 / 8) * 2048 + ptx::sw128(r, unit16 % 8),
+      ptx::cp_async16_zfill(qs_u32 + buf * (CH * 2048) + (unit16 / 8) * 2048 + ptx::sw128(lane >> 1, unit16 % 8),
                             src + 8 * unit16, valid);
     }
     ptx::cp_async_commit();
-  };
-  auto fetch_meta = [&](const Unit& un) {
-    RowMeta m{{0, 0, 0}, {0, 0, 0}, INT32_MIN, INT32_MIN};
-    if (g8 < un.n_rows) {
-      m.r0 = row_info(p, un, g8);
-      m.pos0 = p.tok_pos[m.r0.token];
-    }
-    if (g8 + 8 < un.n_rows) {
-      m.r1 = row_info(p, un, g8 + 8);
-      m.pos1 = p.tok_pos[m.r1.token];
-    }
-    return m;
+    return r;
   };
 
-  int ui = blockIdx.x * SW_WARPS + warp;
-  Unit u_next = ui < p.n_units ? p.units[ui] : Unit{};
-  RowMeta meta_next{};
-  if (ui < p.n_units) {
-    fetch_q(u_next, 0);
-    meta_next = fetch_meta(u_next);
-  }
-  for (int buf = 0; ui < p.n_units; ui += wstride, buf ^= 1) {
-    const Unit u = u_next;
-    const RowMeta meta = meta_next;
+  int nidx = next_index();
+  Pre pre{};
+  if (nidx < p.n_units) pre = prefetch(nidx, 0);
+  for (int buf = 0; nidx < p.n_units; buf ^= 1) {
+    const Pre cu = pre;
     ptx::cp_async_wait_group0();
     __syncwarp();
     uint32_t qa[D / 16][4];
@@ -229,25 +225,30 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
                    qa[kk][1], qa[kk][2], qa[kk][3]);
     }
     __syncwarp();   // every lane's ldmatrix of this buffer is done before the next prefetch targets it later
-    if (ui + wstride < p.n_units) {
-      u_next = p.units[ui + wstride];
-      fetch_q(u_next, buf ^ 1);
-      meta_next = fetch_meta(u_next);
-    }
-    const RowInfo ri0 = meta.r0, ri1 = meta.r1;
-    const int32_t pos0r = meta.pos0, pos1r = meta.pos1;
+    nidx = next_index();
+    if (nidx < p.n_units) pre = prefetch(nidx, buf ^ 1);
+    const int32_t pos0r = cu.d0.qrow >= 0 ? cu.d0.pos : INT32_MIN;
+    const int32_t pos1r = cu.d1.qrow >= 0 ? cu.d1.pos : INT32_MIN;
 
     float o[NT][4];
 #pragma unroll
     for (int j = 0; j < NT; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
     float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
 
-    for (int e = u.entry_begin; e < u.entry_end; ++e) {
-      const KvEntry en = p.entries[e];
-      for (int h = 0; h * SW_KEYS < en.count; ++h, ++it) {
+    int4 eb_cur = cu.ebatch, eb_nxt = make_int4(0, 0, 0, 0);
+    if (cu.ne > 32) eb_nxt = lane + 32 < cu.ne ? ents[cu.eb + 32 + lane] : make_int4(0, 0, 0, 0);
+    for (int k = 0; k < cu.ne; ++k) {
+      const int kl = k & 31;
+      if (kl == 0 && k > 0) {   // next batch of 32 entries (prefetched one batch ahead)
+        eb_cur = eb_nxt;
+        if (k + 32 < cu.ne) eb_nxt = lane + k + 32 < cu.ne ? ents[cu.eb + k + 32 + lane] : make_int4(0, 0, 0, 0);
+      }
+      const int en_pos0 = __shfl_sync(0xffffffffu, eb_cur.z, kl);
+      const int en_count = __shfl_sync(0xffffffffu, eb_cur.w, kl);
+      for (int h = 0; h * SW_KEYS < en_count; ++h, ++it) {
         const uint32_t s = it % SW_STAGES, ph = (it / SW_STAGES) & 1;
         const int kbase = h * SW_KEYS;                 // slot of key 0 of this stage
-        const int nvalid = en.count - kbase;           // >= 1
+        const int nvalid = en_count - kbase;           // >= 1
         ptx::mbar_wait(&wfull[s], ph);
         const uint32_t kst = ptx::smem_u32(ring + s * L.stage_stride);
         const uint32_t vst = kst + CH * SW_CHUNK;
@@ -276,7 +277,7 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
             const int key = nt * 8 + 2 * c4 + c;          // key within the stage
-            const int kp = en.pos0 + kbase + key;
+            const int kp = en_pos0 + kbase + key;
             const bool kv = key < nvalid;
             sc[nt][c] = (kv && kp <= pos0r) ? sc[nt][c] * p.scale_log2 : -INFINITY;
             sc[nt][2 + c] = (kv && kp <= pos1r) ? sc[nt][2 + c] * p.scale_log2 : -INFINITY;
@@ -341,28 +342,25 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
     l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
 #pragma unroll
     for (int half_row = 0; half_row < 2; ++half_row) {
-      const int r = g8 + 8 * half_row;
-      if (r >= u.n_rows) continue;
-      const RowInfo ri = half_row ? ri1 : ri0;
+      const RowDesc d = half_row ? cu.d1 : cu.d0;
+      if (d.qrow < 0 || d.target == PM_SKIP) continue;
       const float l = half_row ? l1 : l0, m = half_row ? m1 : m0;
-      const int32_t tgt = row_target(p, u, ri.tl);
-      if (tgt == PM_SKIP) continue;
       const float inv = l > 0.f ? 1.f / l : 0.f;
       const float lse2 = l > 0.f ? (m == -INFINITY ? 0.f : m) + log2f(l) : -INFINITY;
-      if (tgt == PM_DIRECT) {
-        __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.out) + ((int64_t)ri.token * p.hq + ri.head) * D;
+      if (d.target == PM_DIRECT) {
+        __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.out) + (int64_t)d.qrow * D;
 #pragma unroll
         for (int j = 0; j < NT; ++j)
           *reinterpret_cast<uint32_t*>(dst + 8 * j + 2 * c4) =
               ptx::pack_bf16(o[j][2 * half_row] * inv, o[j][2 * half_row + 1] * inv);
-        if (c4 == 0) p.lse[(int64_t)ri.token * p.hq + ri.head] = lse2 * kLn2;
+        if (c4 == 0) p.lse[d.qrow] = lse2 * kLn2;
       } else {
-        float* dst = p.ws_o + ((int64_t)tgt * p.hq + ri.head) * D;
+        float* dst = p.ws_o + ((int64_t)d.target * p.hq + d.head) * D;
 #pragma unroll
         for (int j = 0; j < NT; ++j)
           *reinterpret_cast<float2*>(dst + 8 * j + 2 * c4) =
               make_float2(o[j][2 * half_row] * inv, o[j][2 * half_row + 1] * inv);
-        if (c4 == 0) p.ws_lse[(int64_t)tgt * p.hq + ri.head] = lse2;
+        if (c4 == 0) p.ws_lse[(int64_t)d.target * p.hq + d.head] = lse2;
       }
     }
   }

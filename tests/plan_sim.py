@@ -16,7 +16,7 @@ from oracle import attention as A
 from synth import values as V
 
 SEC = ["tok_pos", "item_tok_off", "item_tokens", "entries", "dunits", "sunits", "partmap",
-       "merge_tok", "merge_off", "merge_rows"]
+       "merge_tok", "merge_off", "merge_rows", "stream_rows"]
 
 
 def plan_image(tree):
@@ -31,13 +31,34 @@ def plan_image(tree):
     blob = np.ctypeslib.as_array(C.cast(data, C.POINTER(C.c_uint8)), (nbytes.value,)).copy() \
         if nbytes.value else np.zeros(0, np.uint8)
     secs = {}
-    width = {"entries": 4, "dunits": 8, "sunits": 8}
+    width = {"entries": 4, "dunits": 8, "sunits": 8, "stream_rows": 4}
     for i, name in enumerate(SEC):
         o, n = int(off[i]), int(cnt[i])
         k = width.get(name, 1)
         secs[name] = blob[o:o + 4 * n * k].view(np.int32).reshape(n, k) if k > 1 else \
             blob[o:o + 4 * n].view(np.int32)
     return secs
+
+
+STREAM_ROWS = 16
+
+
+def check_stream_rows(P, g, Hq):
+    """The planner's per-row descriptors of streaming units restate (item row ->
+    token, head, position, partmap target) exactly."""
+    sr = P["stream_rows"]
+    assert len(sr) == STREAM_ROWS * len(P["sunits"])
+    for ui, u in enumerate(P["sunits"]):
+        item, kvh, rb, nr, eb, ee, pmb, tb = (int(x) for x in u)
+        for r in range(STREAM_ROWS):
+            qrow, pos, tgt, head = (int(x) for x in sr[ui * STREAM_ROWS + r])
+            if r >= nr:
+                assert qrow == -1 and tgt == -2
+                continue
+            tl, j = (rb + r) // g, (rb + r) % g
+            tok = int(P["item_tokens"][tb + tl])
+            assert (qrow, pos, tgt, head) == (tok * Hq + kvh * g + j, int(P["tok_pos"][tok]),
+                                              int(P["partmap"][pmb + tl]), kvh * g + j)
 
 
 def simulate(w, tree):
@@ -60,6 +81,7 @@ def simulate(w, tree):
     written = np.zeros((T, Hq), dtype=np.int64)
     fused = {}
     dense_rows = set()
+    check_stream_rows(P, g, Hq)
     for kind, units in (("dense", P["dunits"]), ("stream", P["sunits"])):
         for u in units:
             item, kvh, rb, nr, eb, ee, pmb, tb = (int(x) for x in u)
