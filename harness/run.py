@@ -98,7 +98,7 @@ def device_batch(w, device="cuda", tree_kw=None, n_cache_pages=None, fill=True) 
     q = torch.zeros((T, w.num_q_heads, w.head_dim), dtype=dt, device=device)
     out = torch.zeros_like(q)
     lse = torch.zeros((T, w.num_q_heads), dtype=torch.float32, device=device)
-    ws = torch.empty(max(256, tree.workspace_bytes), dtype=torch.uint8, device=device)
+    ws = torch.zeros(max(256, tree.workspace_bytes), dtype=torch.uint8, device=device)   # zeroed once (arrival counters)
     plan_buf = torch.empty(max(256, tree.plan_bytes), dtype=torch.uint8, device=device)
     plan = tree.upload_plan(plan_buf)
     if fill:

@@ -198,9 +198,13 @@ typedef struct {
   int64_t n_cache_pages;     /* pages in the cache allocations (page ids must be < this)     */
   void* out;                 /* device [sum q, Hq, D] (kv dtype), written                    */
   float* lse;                /* device [sum q, Hq] fp32 natural-log LSE, written             */
-  void* workspace;           /* device, >= blend_workspace_bytes (always required), contents
-                                scratch: partial (o, lse) rows + the streaming pass's unit
-                                counter; one call in flight per workspace                    */
+  void* workspace;           /* device, >= blend_workspace_bytes (always required): partial
+                                (o, lse) rows, the streaming pass's unit counter and the
+                                arrival counters [merge list][Hq] with which the last
+                                producer of a (token, head) merges it (no merge launch).
+                                ZERO-FILL IT ONCE after allocation; every completed call
+                                leaves the counters at zero again.  One call in flight per
+                                workspace                                                   */
   size_t workspace_bytes;
   const blend_plan* plan;    /* from blend_plan_upload (its buffer must be resident)         */
   int32_t path;              /* BLEND_PATH_*: AUTO = tcgen05 dense + streaming (+ generic for
@@ -210,7 +214,9 @@ typedef struct {
                                 streaming pass is launched with programmatic dependent launch
                                 and overlaps the dense pass on free SMs (the two passes are
                                 independent; the streaming grid completes only after the
-                                dense grid, so the merge sees both)                        */
+                                dense grid).  Partials with several sources are merged by
+                                their last producer (arrival counters in the workspace);
+                                the merge kernel runs only on the GENERIC / fp32 paths   */
   void* events[4];           /* optional cudaEvent_t recorded before dense, before stream,
                                 before merge, after merge (NULL entries skipped); non-NULL
                                 events[1] or events[2] imply BLEND_SERIALIZE                 */

@@ -81,7 +81,8 @@ extern "C" int blend_attention(const blend_attn_args* a, void* stream) {
   const int hq = pl.num_q_heads, D = pl.head_dim;
   size_t o_bytes = ((size_t)prow * hq * D * 4 + 255) & ~size_t(255);
   const size_t lse_bytes = ((size_t)prow * hq * 4 + 255) & ~size_t(255);
-  const size_t need = o_bytes + lse_bytes + 256;   // + the streaming pass's unit counter
+  const size_t arr_bytes = ((size_t)pl.count[SEC_MERGE_TOK] * hq * 4 + 255) & ~size_t(255);
+  const size_t need = o_bytes + lse_bytes + 256 + arr_bytes;   // + unit counter + arrival counters
   if (!a->workspace || a->workspace_bytes < need)
     return blend_internal_fail(BLEND_ENOSPC, "attention: workspace too small");
   if (a->n_cache_pages <= 0) return blend_internal_fail(BLEND_EINVAL, "attention: n_cache_pages");
@@ -104,6 +105,7 @@ extern "C" int blend_attention(const blend_attn_args* a, void* stream) {
   p.merge_off = (const int32_t*)(base + pl.off[SEC_MERGE_OFF]);
   p.merge_rows = (const int32_t*)(base + pl.off[SEC_MERGE_ROWS]);
   p.srows = (const RowDesc*)(base + pl.off[SEC_STREAM_ROWS]);
+  p.prow_list = (const int32_t*)(base + pl.off[SEC_PROW_LIST]);
   p.n_merge = (int32_t)pl.count[SEC_MERGE_TOK];
   p.hq = hq;
   p.hkv = pl.num_kv_heads;
@@ -130,6 +132,13 @@ extern "C" int blend_attention(const blend_attn_args* a, void* stream) {
   // sees 0); without that kernel a memset ahead of the passes does.
   const bool stream_dyn = !generic && pl.count[SEC_STREAM_UNITS] > 0 && n_merge_all == n_merge_unfused;
   const bool dense_tc = !generic && a->path != BLEND_PATH_NO_TCGEN05 && pd.n_units > 0;
+  // Arrival merging: when every partial is produced by the tcgen05 dense kernel or the
+  // warp streaming kernel, the last producer of each (token, head) merges it and the
+  // merge launch disappears (no grid-completion dependency at the end of the step).
+  const bool arrival = !generic && n_merge_all == n_merge_unfused &&
+                       (pd.n_units == 0 || a->path != BLEND_PATH_NO_TCGEN05);
+  int32_t* arrive = arrival ? (int32_t*)((char*)a->workspace + o_bytes + lse_bytes + 256) : nullptr;
+  pd.arrive = arrive;
   pd.sched = stream_dyn && dense_tc ? p.sched : nullptr;
   if (stream_dyn && !dense_tc) {
     e = cudaMemsetAsync(p.sched, 0, sizeof(int32_t), st);
@@ -144,6 +153,7 @@ extern "C" int blend_attention(const blend_attn_args* a, void* stream) {
   ps_.units = (const Unit*)(base + pl.off[SEC_STREAM_UNITS]);
   ps_.n_units = (int32_t)pl.count[SEC_STREAM_UNITS];
   ps_.avg_entries = ps_.n_units > 0 ? (int32_t)(pl.count[SEC_COUNT + 1] / ps_.n_units) : 0;
+  ps_.arrive = arrive;
   if (generic) e = launch_generic(ps_, st);
   else if (n_merge_all != n_merge_unfused) e = launch_stream(ps_, a->n_cache_pages, st, overlap);   // fused merges
   else e = launch_streamw(ps_, a->n_cache_pages, st, overlap);
@@ -152,8 +162,10 @@ extern "C" int blend_attention(const blend_attn_args* a, void* stream) {
   if (a->events[2]) cudaEventRecord((cudaEvent_t)a->events[2], st);
   AttnParams pm = p;
   pm.n_merge = (int32_t)pl.count[SEC_COUNT + 2];   // fused lists are merged by the streaming pass
-  e = launch_merge(pm, st, overlap);
-  if (e != cudaSuccess) return cuda_fail(e);
+  if (!arrival) {
+    e = launch_merge(pm, st, overlap);
+    if (e != cudaSuccess) return cuda_fail(e);
+  }
   if (a->events[3]) cudaEventRecord((cudaEvent_t)a->events[3], st);
   e = cudaPeekAtLastError();
   if (e != cudaSuccess) return cuda_fail(e);

@@ -36,6 +36,8 @@ struct AttnParams {
   int32_t avg_entries;   // host-side launch heuristic: mean entries per unit
   const RowDesc* srows;  // streaming units' row descriptors (SEC_STREAM_ROWS)
   int32_t* sched;        // workspace word: dynamic unit counter of the streaming pass (zeroed per call)
+  const int32_t* prow_list;   // partial row -> {merge list, source count} (SEC_PROW_LIST)
+  int32_t* arrive;       // arrival counters [merge list][Hq] (workspace; NULL: the merge kernel merges)
 };
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
@@ -111,6 +113,94 @@ __device__ __forceinline__ void fused_merge_store(const AttnParams& p, int32_t t
   for (int k = 0; k < 16; ++k)
     if (k < n) st_elem(p.out, ob + e0 + k * stride, acc[k] * inv, p.kv_f32);
   if (write_lse) p.lse[(int64_t)token * p.hq + head] = M != -INFINITY ? (M + log2f(tot)) * kLn2 : -INFINITY;
+}
+
+// LSE merge of merge list m, q head h by one warp (reading #17: the list's fixed
+// ascending key-start order, so the result does not depend on who merges or when);
+// lanes own D/32 contiguous elements.  Partials are read through L2 (ld.global.cg):
+// with arrival merging they were written by other SMs during this launch.
+__device__ __forceinline__ void warp_merge_row(const AttnParams& p, int m, int h, int lane) {
+  const int token = p.merge_tok[m];
+  const int s0 = p.merge_off[m], s1 = p.merge_off[m + 1];
+  const int D = p.d;
+  const int vec = D / 32;          // 2 or 4 elements per lane
+  const int e0 = lane * vec;
+  // One pass in chunks of MCH sources: every load of a chunk is issued before any is
+  // used (rows -> lse -> o are the only dependent steps), then an online rescale.
+  constexpr int MCH = 4;
+  float mx = -INFINITY, tot = 0.f;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int c0 = s0; c0 < s1; c0 += MCH) {
+    int64_t row[MCH];
+    float l[MCH];
+    float4 v[MCH];
+#pragma unroll
+    for (int i = 0; i < MCH; ++i) row[i] = c0 + i < s1 ? (int64_t)p.merge_rows[c0 + i] : -1;
+#pragma unroll
+    for (int i = 0; i < MCH; ++i) l[i] = row[i] >= 0 ? __ldcg(p.ws_lse + row[i] * p.hq + h) : -INFINITY;
+#pragma unroll
+    for (int i = 0; i < MCH; ++i) {
+      v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (row[i] >= 0) {
+        const float* src = p.ws_o + (row[i] * p.hq + h) * D + e0;
+        if (vec == 4) {
+          v[i] = __ldcg(reinterpret_cast<const float4*>(src));
+        } else {
+          const float2 t = __ldcg(reinterpret_cast<const float2*>(src));
+          v[i].x = t.x;
+          v[i].y = t.y;
+        }
+      }
+    }
+    float cm = mx;
+#pragma unroll
+    for (int i = 0; i < MCH; ++i) cm = fmaxf(cm, l[i]);
+    if (cm == -INFINITY) continue;
+    const float a = exp2f(mx - cm);      // mx = -inf on the first live chunk -> 0
+    tot *= a;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc[k] *= a;
+#pragma unroll
+    for (int i = 0; i < MCH; ++i) {
+      const float w = exp2f(l[i] - cm);  // l = -inf (absent source) -> 0
+      tot += w;
+      acc[0] = fmaf(w, v[i].x, acc[0]);
+      acc[1] = fmaf(w, v[i].y, acc[1]);
+      acc[2] = fmaf(w, v[i].z, acc[2]);
+      acc[3] = fmaf(w, v[i].w, acc[3]);
+    }
+    mx = cm;
+  }
+  const float inv = tot > 0.f ? 1.f / tot : 0.f;
+  const int64_t ob = ((int64_t)token * p.hq + h) * D + e0;
+  for (int k = 0; k < vec; ++k) st_elem(p.out, ob + k, acc[k] * inv, p.kv_f32);
+  if (lane == 0) p.lse[(int64_t)token * p.hq + h] = mx != -INFINITY ? (mx + log2f(tot)) * kLn2 : -INFINITY;
+}
+
+// Arrival merging ("the last producer merges", replaces the merge launch): a thread
+// that has written partial row tgt of q head h (and fenced it) counts itself in;
+// returns true for the last of the list's n sources, which then owns the merge.  The
+// counter is left at 0 for the next call (the workspace counters start zeroed).
+__device__ __forceinline__ bool arrive_last(const AttnParams& p, int32_t m, int32_t h, int32_t nsrc) {
+  int32_t* c = p.arrive + (int64_t)m * p.hq + h;
+  const bool last = atomicAdd(c, 1) == nsrc - 1;
+  if (last) {
+    *c = 0;
+    __threadfence();   // acquire side: the other sources' partials are read after this
+  }
+  return last;
+}
+
+// Warp-wide: every lane with last = true has its (m, h) merged by the whole warp.
+__device__ __forceinline__ void warp_merge_flagged(const AttnParams& p, bool last, int m, int h, int lane) {
+  uint32_t lm = __ballot_sync(0xffffffffu, last);
+  __syncwarp();
+  while (lm) {
+    const int src = __ffs(lm) - 1;
+    lm &= lm - 1;
+    const int mm = __shfl_sync(0xffffffffu, m, src), hh = __shfl_sync(0xffffffffu, h, src);
+    warp_merge_row(p, mm, hh, lane);
+  }
 }
 
 }  // namespace blend

@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
     const uint32_t lane_base = (uint32_t)(((warp - 4) & 3) * 32) << 16;
     const uint32_t col_o = 256 + t * D;
     uint32_t sb = 0;                                  // blocks of this tile processed so far
-    uint32_t scnt[2] = {0, 0};                        // s_full completions consumed per S buffer
+    uint32_t scnt0 = 0, scnt1 = 0;                    // s_full completions consumed per S buffer (registers)
     int2 enext[EPB];                                  // {pos0, count} of the next block's entries
     auto load_meta = [&](const Unit& un, int j) {
 #pragma unroll
@@ -294,9 +294,13 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         tgt = row_target(p, u, ri.tl);
       }
       float m_ref = -INFINITY, l = 0.f;
+      int2 am = make_int2(-1, 0);                     // {merge list, sources} of a partial row
       load_meta(u, 0);
       for (int j = 0; j < nb; ++j, ++sb) {
         const int buf = j & 1;
+        // arrival-merge metadata, loaded during the unit's last block (used after its PV)
+        if (j == nb - 1 && p.arrive != nullptr && tgt >= 0)
+          am = *reinterpret_cast<const int2*>(p.prow_list + 2 * tgt);
         const uint32_t col_s = t * 128 + buf * DN_KB;
         // key positions of this block from the stage metadata the producer wrote (the
         // stage cannot be refilled before this block's P is consumed)
@@ -315,7 +319,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
           vis[i] = v;
           full_vis = full_vis && (v == BOX);
         }
-        ptx::mbar_wait(&s_full[t * 2 + buf], (scnt[buf]++) & 1);   // per-buffer completion count
+        ptx::mbar_wait(&s_full[t * 2 + buf], (buf ? scnt1++ : scnt0++) & 1);   // per-buffer completion count
         ptx::tc_fence_after();
         float sv[DN_KB];
         ptx::tmem_ld32(tmem + lane_base + col_s, reinterpret_cast<uint32_t*>(sv));
@@ -339,7 +343,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
           // previous completion on this barrier (PV(j-3)) is certified by s_full(j-1) and
           // PV(j+1) cannot be issued before this block's P.
           const int pb_ = (j - 1) & 1;
-          ptx::mbar_wait(&o_done[t * 2 + pb_], (scnt[pb_] - 1) & 1);
+          ptx::mbar_wait(&o_done[t * 2 + pb_], ((pb_ ? scnt1 : scnt0) - 1) & 1);
           ptx::tc_fence_after();
           const float alpha = need ? ptx::ex2(m_ref - mx2) : 1.f;
 #pragma unroll 1
@@ -397,7 +401,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       // this also certifies every earlier PV of the unit)
       {
         const int lb = (nb - 1) & 1;
-        ptx::mbar_wait(&o_done[t * 2 + lb], (scnt[lb] - 1) & 1);
+        ptx::mbar_wait(&o_done[t * 2 + lb], ((lb ? scnt1 : scnt0) - 1) & 1);
       }
       ptx::tc_fence_after();
       const float m_use = m_ref == -INFINITY ? 0.f : m_ref;
@@ -430,6 +434,14 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       }
       if (tgt == PM_DIRECT) p.lse[(int64_t)token * p.hq + head] = lse2 * kLn2;
       else if (tgt >= 0) p.ws_lse[(int64_t)tgt * p.hq + head] = lse2;
+      if (p.arrive != nullptr) {   // the last producer of a (token, head) merges it (no merge launch)
+        bool last = false;
+        if (tgt >= 0) {
+          __threadfence();
+          last = arrive_last(p, am.x, head, am.y);
+        }
+        warp_merge_flagged(p, last, am.x, head, lane);
+      }
       ptx::tc_fence_before();
     }
   }

@@ -149,65 +149,9 @@ __global__ void __launch_bounds__(128) generic_unit_kernel(AttnParams p) {
 // One warp per (merged token, q head); lanes own D/32 contiguous elements.
 __global__ void __launch_bounds__(256) merge_kernel(AttnParams p) {
   ptx::pdl_wait();   // launched as a programmatic dependent of the streaming pass
-  const int m = blockIdx.x;
   const int h = blockIdx.y * 8 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
   if (h >= p.hq) return;
-  const int token = p.merge_tok[m];
-  const int s0 = p.merge_off[m], s1 = p.merge_off[m + 1];
-  const int D = p.d;
-  const int vec = D / 32;          // 2 or 4 elements per lane
-  const int e0 = lane * vec;
-  // One pass in chunks of MCH sources: every load of a chunk is issued before any is
-  // used (rows -> lse -> o are the only dependent steps), then an online rescale.
-  constexpr int MCH = 4;
-  float mx = -INFINITY, tot = 0.f;
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int c0 = s0; c0 < s1; c0 += MCH) {
-    int64_t row[MCH];
-    float l[MCH];
-    float4 v[MCH];
-#pragma unroll
-    for (int i = 0; i < MCH; ++i) row[i] = c0 + i < s1 ? (int64_t)p.merge_rows[c0 + i] : -1;
-#pragma unroll
-    for (int i = 0; i < MCH; ++i) l[i] = row[i] >= 0 ? p.ws_lse[row[i] * p.hq + h] : -INFINITY;
-#pragma unroll
-    for (int i = 0; i < MCH; ++i) {
-      v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (row[i] >= 0) {
-        const float* src = p.ws_o + (row[i] * p.hq + h) * D + e0;
-        if (vec == 4) {
-          v[i] = *reinterpret_cast<const float4*>(src);
-        } else {
-          const float2 t = *reinterpret_cast<const float2*>(src);
-          v[i].x = t.x;
-          v[i].y = t.y;
-        }
-      }
-    }
-    float cm = mx;
-#pragma unroll
-    for (int i = 0; i < MCH; ++i) cm = fmaxf(cm, l[i]);
-    if (cm == -INFINITY) continue;
-    const float a = exp2f(mx - cm);      // mx = -inf on the first live chunk -> 0
-    tot *= a;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) acc[k] *= a;
-#pragma unroll
-    for (int i = 0; i < MCH; ++i) {
-      const float w = exp2f(l[i] - cm);  // l = -inf (absent source) -> 0
-      tot += w;
-      acc[0] = fmaf(w, v[i].x, acc[0]);
-      acc[1] = fmaf(w, v[i].y, acc[1]);
-      acc[2] = fmaf(w, v[i].z, acc[2]);
-      acc[3] = fmaf(w, v[i].w, acc[3]);
-    }
-    mx = cm;
-  }
-  const float inv = tot > 0.f ? 1.f / tot : 0.f;
-  const int64_t ob = ((int64_t)token * p.hq + h) * D + e0;
-  for (int k = 0; k < vec; ++k) st_elem(p.out, ob + k, acc[k] * inv, p.kv_f32);
-  if (lane == 0) p.lse[(int64_t)token * p.hq + h] = mx != -INFINITY ? (mx + log2f(tot)) * kLn2 : -INFINITY;
+  warp_merge_row(p, blockIdx.x, h, threadIdx.x & 31);
 }
 
 cudaError_t set_smem_once(const void* func, size_t bytes);

@@ -733,7 +733,14 @@ int build_plan(blend_tree* t) {
   // kernel gets each row's q/out row, position and partmap target in one load
   // instead of the item_tokens -> tok_pos / partmap chain.
   std::vector<blend::RowDesc> srows(sunits.size() * blend::STREAM_ROWS,
-                                    blend::RowDesc{-1, INT32_MIN, blend::PM_SKIP, -1});
+                                    blend::RowDesc{-1, INT32_MIN, blend::PM_SKIP, -1, -1, 0, 0, 0});
+  std::vector<int32_t> prow_list(2 * prow, -1);   // partial row -> {merge list, its source count}
+  for (size_t m = 0; m + 1 < merge_off.size(); ++m)
+    for (int32_t s_ = merge_off[m]; s_ < merge_off[m + 1]; ++s_)
+      if (merge_rows[s_] >= 0) {
+        prow_list[2 * merge_rows[s_]] = (int32_t)m;
+        prow_list[2 * merge_rows[s_] + 1] = merge_off[m + 1] - merge_off[m];
+      }
   {
     const int32_t g = a.num_q_heads / a.num_kv_heads;
     for (size_t ui = 0; ui < sunits.size(); ++ui) {
@@ -746,6 +753,10 @@ int build_plan(blend_tree* t) {
         d.pos = tok_pos[tok];
         d.target = partmap[u.pm_base + tl];
         d.head = u.kvh * g + j;
+        if (d.target >= 0) {
+          d.mlist = prow_list[2 * d.target];
+          d.nsrc = prow_list[2 * d.target + 1];
+        }
       }
     }
   }
@@ -772,12 +783,15 @@ int build_plan(blend_tree* t) {
   put(SEC_MERGE_OFF, merge_off.data(), 4, merge_off.size());
   put(SEC_MERGE_ROWS, merge_rows.data(), 4, merge_rows.size());
   put(SEC_STREAM_ROWS, srows.data(), sizeof(RowDesc), srows.size());
+  put(SEC_PROW_LIST, prow_list.data(), 4, prow_list.size());
   blob.resize((blob.size() + 255) & ~size_t(255));
 
   t->n_partial_rows = prow;
   const size_t hq = a.num_q_heads, D = a.head_dim;
   size_t o_bytes = ((size_t)prow * hq * D * 4 + 255) & ~size_t(255);
-  t->workspace_bytes = o_bytes + (((size_t)prow * hq * 4 + 255) & ~size_t(255)) + 256;   // + unit counter
+  // partials o | lse | unit counter (256 B) | arrival counters [merge list][Hq]
+  t->workspace_bytes = o_bytes + (((size_t)prow * hq * 4 + 255) & ~size_t(255)) + 256 +
+                       (((size_t)merge_tok.size() * hq * 4 + 255) & ~size_t(255));
   t->info.n_tokens = T;
   t->info.n_items = (int64_t)items.size();
   t->info.n_dense_units = (int64_t)dunits.size();

@@ -367,22 +367,34 @@ __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
 }
-// 2^x for a pair on the FMA/ALU pipes: 2^floor(x) * p(frac), degree-3 minimax p
-// (max rel. error ~9e-5); x is clamped at -127 (result ~1e-38, i.e. 0 for softmax).
+__device__ __forceinline__ uint64_t fadd2_rm(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// 2^x for a pair without the XU pipe (which the MUFU exponentials saturate): the
+// floor comes from a round-toward-minus-infinity add of 1.5*2^23 (FADD2, FMA pipe),
+// 2^frac from a degree-3 minimax polynomial (3 FFMA2, max rel. error ~9e-5), and
+// the exponent is added to the bits with one IMAD per element.  x is clamped at -127
+// (result ~1e-38, i.e. 0 for softmax).  floorf / float->int conversions would run
+// on XU (FRND / F2I) and cost more XU slots than the MUFU.EX2 they replace.
 __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x2) {
+  constexpr float kMagic = 12582912.0f;   // 1.5 * 2^23: ulp 1, so MAGIC + floor(x) is exact
   float a, b;
   f2unpack(x2, a, b);
-  a = fmaxf(a, -127.f);
-  b = fmaxf(b, -127.f);
-  const float fa = floorf(a), fb = floorf(b);
-  const uint64_t f = fadd2(f2pack(a, b), f2pack(-fa, -fb));
+  const uint64_t xc = f2pack(fmaxf(a, -127.f), fmaxf(b, -127.f));
+  const uint64_t j = fadd2_rm(xc, f2pack(kMagic, kMagic));              // MAGIC + floor(x)
+  const uint64_t fl = fadd2(j, f2pack(-kMagic, -kMagic));                // floor(x), exact
+  const uint64_t f = ffma2(fl, f2pack(-1.f, -1.f), xc);                  // x - floor(x) in [0, 1)
   uint64_t p = ffma2(f, f2pack(0.0790f, 0.0790f), f2pack(0.2243f, 0.2243f));
   p = ffma2(p, f, f2pack(0.6967f, 0.6967f));
   p = ffma2(p, f, f2pack(1.0f, 1.0f));
-  float pa, pb;
+  float pa, pb, ja, jb;
   f2unpack(p, pa, pb);
-  pa = __int_as_float(__float_as_int(pa) + ((int)fa << 23));
-  pb = __int_as_float(__float_as_int(pb) + ((int)fb << 23));
+  f2unpack(j, ja, jb);
+  // bits(MAGIC + n) << 23 == n << 23 (mod 2^32): the exponent field gains floor(x)
+  pa = __int_as_float(__float_as_int(pa) + (__float_as_int(ja) << 23));
+  pb = __int_as_float(__float_as_int(pb) + (__float_as_int(jb) << 23));
   return f2pack(pa, pb);
 }
 }  // namespace ptx

@@ -363,6 +363,18 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
         if (c4 == 0) p.ws_lse[(int64_t)d.target * p.hq + d.head] = lse2;
       }
     }
+    if (p.arrive != nullptr &&
+        __any_sync(0xffffffffu, (cu.d0.qrow >= 0 && cu.d0.target >= 0) || (cu.d1.qrow >= 0 && cu.d1.target >= 0))) {
+      // arrival merging: the last producer of each (token, head) merges its list
+      __threadfence();   // this lane's partial stores, before the row's count-in
+      __syncwarp();
+#pragma unroll
+      for (int half_row = 0; half_row < 2; ++half_row) {
+        const RowDesc d = half_row ? cu.d1 : cu.d0;
+        const bool last = c4 == 0 && d.qrow >= 0 && d.target >= 0 && arrive_last(p, d.mlist, d.head, d.nsrc);
+        warp_merge_flagged(p, last, d.mlist, d.head, lane);
+      }
+    }
   }
   ptx::pdl_wait();
 }

@@ -16,7 +16,7 @@ from oracle import attention as A
 from synth import values as V
 
 SEC = ["tok_pos", "item_tok_off", "item_tokens", "entries", "dunits", "sunits", "partmap",
-       "merge_tok", "merge_off", "merge_rows", "stream_rows"]
+       "merge_tok", "merge_off", "merge_rows", "stream_rows", "prow_list"]
 
 
 def plan_image(tree):
@@ -31,12 +31,13 @@ def plan_image(tree):
     blob = np.ctypeslib.as_array(C.cast(data, C.POINTER(C.c_uint8)), (nbytes.value,)).copy() \
         if nbytes.value else np.zeros(0, np.uint8)
     secs = {}
-    width = {"entries": 4, "dunits": 8, "sunits": 8, "stream_rows": 4}
+    width = {"entries": 4, "dunits": 8, "sunits": 8, "stream_rows": 8}
     for i, name in enumerate(SEC):
         o, n = int(off[i]), int(cnt[i])
         k = width.get(name, 1)
         secs[name] = blob[o:o + 4 * n * k].view(np.int32).reshape(n, k) if k > 1 else \
             blob[o:o + 4 * n].view(np.int32)
+    secs["prow_list"] = secs["prow_list"].reshape(-1, 2)
     return secs
 
 
@@ -48,17 +49,23 @@ def check_stream_rows(P, g, Hq):
     token, head, position, partmap target) exactly."""
     sr = P["stream_rows"]
     assert len(sr) == STREAM_ROWS * len(P["sunits"])
+    mo = P["merge_off"]
     for ui, u in enumerate(P["sunits"]):
         item, kvh, rb, nr, eb, ee, pmb, tb = (int(x) for x in u)
         for r in range(STREAM_ROWS):
-            qrow, pos, tgt, head = (int(x) for x in sr[ui * STREAM_ROWS + r])
+            qrow, pos, tgt, head, ml, ns = (int(x) for x in sr[ui * STREAM_ROWS + r][:6])
             if r >= nr:
-                assert qrow == -1 and tgt == -2
+                assert qrow == -1 and tgt == -2 and ml == -1
                 continue
             tl, j = (rb + r) // g, (rb + r) % g
             tok = int(P["item_tokens"][tb + tl])
             assert (qrow, pos, tgt, head) == (tok * Hq + kvh * g + j, int(P["tok_pos"][tok]),
                                               int(P["partmap"][pmb + tl]), kvh * g + j)
+            if tgt >= 0:   # arrival merging: the row's merge list holds it, with its source count
+                rows = list(P["merge_rows"][mo[ml]:mo[ml + 1]])
+                assert tgt in rows and ns == len(rows) and int(P["merge_tok"][ml]) == tok
+            else:
+                assert ml == -1
 
 
 def simulate(w, tree):
@@ -117,8 +124,13 @@ def simulate(w, tree):
                     if kind == "dense":
                         dense_rows.add(tgt)
     mo = P["merge_off"]
+    pl = P["prow_list"]
+    assert len(pl) == nprow
     for m, tok in enumerate(P["merge_tok"]):
         rows = P["merge_rows"][mo[m]:mo[m + 1]]
+        for r in rows:   # arrival merging: each partial row knows its list and the list's size
+            if r >= 0:
+                assert tuple(int(x) for x in pl[r]) == (m, len(rows))
         real = [r for r in rows if r >= 0]
         assert not np.isnan(part_l[real]).any(), "merge reads an unwritten partial"
         assert sum(1 for r in rows if r < 0) <= 1

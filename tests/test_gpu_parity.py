@@ -225,3 +225,26 @@ def test_c2_fused_merge_and_overlap(fuse, flags):
     db.run(flags=1 - flags)
     torch.cuda.synchronize()
     assert torch.equal(first, db.out)
+
+
+@pytest.mark.parametrize("kw", [dict(), dict(split_tokens=64, dense_split=3)])
+def test_arrival_merge_counters(kw):
+    """Arrival merging: the last producer of each (token, head) merges its list.  Lists
+    with many sources (dense + streaming split-KV), repeated calls on one workspace
+    (the counters must return to zero) and serialised vs overlapped launches all give
+    the same bits, within tolerance of the oracle."""
+    w = W.c2_mmlu_decode(n_req=96)
+    db = device_batch(w, tree_kw=kw)
+    assert db.info["n_merge_tokens"] > 0
+    db.run()
+    torch.cuda.synchronize()
+    _cmp(w, db)
+    first = db.out.clone()
+    n = db.info["n_merge_tokens"] * w.num_q_heads * 4
+    tail = db.ws[db.ws.numel() - ((n + 255) // 256) * 256:]
+    assert int(tail.count_nonzero().item()) == 0, "arrival counters not reset"
+    for flags in (0, 1, 0):
+        db.out.zero_()
+        db.run(flags=flags)
+        torch.cuda.synchronize()
+        assert torch.equal(first, db.out)
