@@ -54,6 +54,23 @@ def load_peaks():
     return d
 
 
+PROFILE_TAG = "r1d"   # profiles/<tag>_ncu.json: ncu --set full captures of this code's kernels
+
+
+def ncu_traffic(workload: str, kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one launch of `kernel` on
+    `workload` from the committed ncu --set full capture (profiles/), or None."""
+    p = os.path.join(ROOT, "profiles", f"{PROFILE_TAG}_ncu.json")
+    try:
+        full = json.load(open(p))["full"]
+    except (OSError, ValueError, KeyError):
+        return None, None
+    d = full.get(f"{workload}_{kernel}")
+    if not d or "traffic_bytes" not in d:
+        return None, None
+    return float(d["traffic_bytes"]), f"profiles/{PROFILE_TAG}_ncu.json [{workload}_{kernel}]"
+
+
 def make_workload(name: str, n_copies: int = 1):
     from synth import workloads as W
     recipes = {"c2": (W.c2_mmlu_decode, 2), "c3": (W.c3_burst_openvid, 3), "c5": (W.c5_70b_32k, 5)}
@@ -339,8 +356,11 @@ def run_ours(args):
         torch.cuda.synchronize()
         gather_ms = g0.elapsed_time(g1)
 
+    # our kernels per timed step: dense + streaming (+ merge: only off the arrival-merge
+    # path, i.e. the generic executor) + the L2 flush between steps
+    arrival = False   # BLEND_ARRIVAL_MERGE is opt-in; the bench runs the default path
     launches_per_step = int(info["n_dense_units"] > 0) + int(info["n_stream_units"] > 0) + \
-        int(info["n_merge_tokens"] > 0)   # merge launch count assumes unfused lists (bench default)
+        int(info["n_merge_tokens"] > 0 and not arrival) + int(do_flush)
 
     # ---- roofline of the dominant kernel (per launch, CUDA events on the launching stream)
     peaks = load_peaks()
@@ -348,16 +368,19 @@ def run_ours(args):
     if md >= mst:
         tf = pw["dense_flops"] / (md * 1e-3) / 1e12
         peak = peaks["bf16_tflops"] if burst else peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+        traffic, tsrc = ncu_traffic(args.workload, "dense_kernel") if path == B.PATH_AUTO else (None, None)
         roof = {"kernel": "dense (tcgen05)" if path == B.PATH_AUTO else "dense (generic executor)",
                 "bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak,
-                "traffic": None, "algorithmic_per_launch": pw["dense_flops"],
+                "traffic": traffic, "traffic_source": tsrc, "algorithmic_per_launch": pw["dense_flops"],
+                "algorithmic_bytes_per_launch": pw["dense_bytes"],
                 "peak_source": peaks["_source"] + (" burst" if burst else " sustained")}
     else:
         gbs = pw["stream_bytes"] / (mst * 1e-3) / 1e9
         peak = peaks["hbm_gbs"]
+        traffic, tsrc = ncu_traffic(args.workload, "streamw_kernel") if path == B.PATH_AUTO else (None, None)
         roof = {"kernel": "stream", "bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s",
-                "frac": gbs / peak, "traffic": None, "algorithmic_per_launch": pw["stream_bytes"],
-                "peak_source": peaks["_source"]}
+                "frac": gbs / peak, "traffic": traffic, "traffic_source": tsrc,
+                "algorithmic_per_launch": pw["stream_bytes"], "peak_source": peaks["_source"]}
 
     line = None
     if rank == 0:

@@ -187,7 +187,7 @@ int blend_plan_upload(const blend_tree* tree, void* dev_buf, size_t bytes, void*
                       blend_plan* plan);
 
 enum { BLEND_PATH_AUTO = 0, BLEND_PATH_GENERIC = 1, BLEND_PATH_NO_TCGEN05 = 2 };
-enum { BLEND_SERIALIZE = 1 };
+enum { BLEND_SERIALIZE = 1, BLEND_ARRIVAL_MERGE = 2 };
 
 typedef struct {
   const void* q;             /* device [sum q, Hq, D] (kv dtype), rows in caller request order:
@@ -214,9 +214,12 @@ typedef struct {
                                 streaming pass is launched with programmatic dependent launch
                                 and overlaps the dense pass on free SMs (the two passes are
                                 independent; the streaming grid completes only after the
-                                dense grid).  Partials with several sources are merged by
-                                their last producer (arrival counters in the workspace);
-                                the merge kernel runs only on the GENERIC / fp32 paths   */
+                                dense grid) and the merge kernel is a programmatic
+                                dependent of the streaming grid.
+                                BLEND_ARRIVAL_MERGE (bf16, AUTO path): no merge launch; the
+                                last producer of each (token, head) merges it, counted in
+                                on the workspace's arrival counters (measured slower than
+                                the merge launch on decode-heavy batches, hence opt-in)  */
   void* events[4];           /* optional cudaEvent_t recorded before dense, before stream,
                                 before merge, after merge (NULL entries skipped); non-NULL
                                 events[1] or events[2] imply BLEND_SERIALIZE                 */

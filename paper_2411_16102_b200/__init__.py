@@ -27,6 +27,7 @@ OK, EINVAL, EMALFORMED, ENOSPC, ECUDA, ENOMEM, EUNSUPPORTED = 0, -1, -2, -3, -4,
 BF16, F32 = 0, 1
 PATH_AUTO, PATH_GENERIC, PATH_NO_TCGEN05 = 0, 1, 2
 SERIALIZE = 1
+ARRIVAL_MERGE = 2
 _DTYPES = {"bf16": BF16, "f32": F32}
 
 

@@ -73,7 +73,7 @@ extern "C" int blend_attention(const blend_attn_args* a, void* stream) {
   const blend_plan& pl = *a->plan;
   if (!pl.dev) return blend_internal_fail(BLEND_EINVAL, "attention: plan not uploaded");
   if (a->path < 0 || a->path > 2) return blend_internal_fail(BLEND_EINVAL, "attention: bad path");
-  if (a->flags & ~BLEND_SERIALIZE) return blend_internal_fail(BLEND_EINVAL, "attention: bad flags");
+  if (a->flags & ~(BLEND_SERIALIZE | BLEND_ARRIVAL_MERGE)) return blend_internal_fail(BLEND_EINVAL, "attention: bad flags");
   static int arch_ok = -1;
   if (arch_ok < 0) arch_ok = check_arch() == BLEND_OK ? 1 : 0;
   if (!arch_ok) return blend_internal_fail(BLEND_EUNSUPPORTED, "libblend is built for sm_100a (B200)");
@@ -81,8 +81,7 @@ extern "C" int blend_attention(const blend_attn_args* a, void* stream) {
   const int hq = pl.num_q_heads, D = pl.head_dim;
   size_t o_bytes = ((size_t)prow * hq * D * 4 + 255) & ~size_t(255);
   const size_t lse_bytes = ((size_t)prow * hq * 4 + 255) & ~size_t(255);
-  const size_t arr_bytes = ((size_t)pl.count[SEC_MERGE_TOK] * hq * 4 + 255) & ~size_t(255);
-  const size_t need = o_bytes + lse_bytes + 256 + arr_bytes;   // + unit counter + arrival counters
+  const size_t need = o_bytes + 2 * lse_bytes + 256;   // + unit counter + arrival counters [prow][Hq]
   if (!a->workspace || a->workspace_bytes < need)
     return blend_internal_fail(BLEND_ENOSPC, "attention: workspace too small");
   if (a->n_cache_pages <= 0) return blend_internal_fail(BLEND_EINVAL, "attention: n_cache_pages");
@@ -132,10 +131,10 @@ extern "C" int blend_attention(const blend_attn_args* a, void* stream) {
   // sees 0); without that kernel a memset ahead of the passes does.
   const bool stream_dyn = !generic && pl.count[SEC_STREAM_UNITS] > 0 && n_merge_all == n_merge_unfused;
   const bool dense_tc = !generic && a->path != BLEND_PATH_NO_TCGEN05 && pd.n_units > 0;
-  // Arrival merging: when every partial is produced by the tcgen05 dense kernel or the
-  // warp streaming kernel, the last producer of each (token, head) merges it and the
-  // merge launch disappears (no grid-completion dependency at the end of the step).
-  const bool arrival = !generic && n_merge_all == n_merge_unfused &&
+  // Arrival merging (opt-in): when every partial is produced by the tcgen05 dense kernel
+  // or the warp streaming kernel, the last producer of each (token, head) merges it and
+  // the merge launch disappears (no grid-completion dependency at the end of the step).
+  const bool arrival = (a->flags & BLEND_ARRIVAL_MERGE) && !generic && n_merge_all == n_merge_unfused &&
                        (pd.n_units == 0 || a->path != BLEND_PATH_NO_TCGEN05);
   int32_t* arrive = arrival ? (int32_t*)((char*)a->workspace + o_bytes + lse_bytes + 256) : nullptr;
   pd.arrive = arrive;

@@ -115,8 +115,10 @@ __device__ __forceinline__ void fused_merge_store(const AttnParams& p, int32_t t
   if (write_lse) p.lse[(int64_t)token * p.hq + head] = M != -INFINITY ? (M + log2f(tot)) * kLn2 : -INFINITY;
 }
 
-// LSE merge of merge list m, q head h by one warp (reading #17: the list's fixed
-// ascending key-start order, so the result does not depend on who merges or when);
+// LSE merge of (unfused) merge list m, q head h by one warp (reading #17: the list's
+// fixed ascending key-start order, so the result does not depend on who merges or when);
+// entry s of an unfused list is partial row s (host planner invariant), so the only
+// dependent loads are merge_off -> partials;
 // lanes own D/32 contiguous elements.  Partials are read through L2 (ld.global.cg):
 // with arrival merging they were written by other SMs during this launch.
 __device__ __forceinline__ void warp_merge_row(const AttnParams& p, int m, int h, int lane) {
@@ -135,7 +137,7 @@ __device__ __forceinline__ void warp_merge_row(const AttnParams& p, int m, int h
     float l[MCH];
     float4 v[MCH];
 #pragma unroll
-    for (int i = 0; i < MCH; ++i) row[i] = c0 + i < s1 ? (int64_t)p.merge_rows[c0 + i] : -1;
+    for (int i = 0; i < MCH; ++i) row[i] = c0 + i < s1 ? (int64_t)(c0 + i) : -1;   // unfused: row s = entry s
 #pragma unroll
     for (int i = 0; i < MCH; ++i) l[i] = row[i] >= 0 ? __ldcg(p.ws_lse + row[i] * p.hq + h) : -INFINITY;
 #pragma unroll
@@ -177,30 +179,71 @@ __device__ __forceinline__ void warp_merge_row(const AttnParams& p, int m, int h
   if (lane == 0) p.lse[(int64_t)token * p.hq + h] = mx != -INFINITY ? (mx + log2f(tot)) * kLn2 : -INFINITY;
 }
 
-// Arrival merging ("the last producer merges", replaces the merge launch): a thread
-// that has written partial row tgt of q head h (and fenced it) counts itself in;
-// returns true for the last of the list's n sources, which then owns the merge.  The
-// counter is left at 0 for the next call (the workspace counters start zeroed).
-__device__ __forceinline__ bool arrive_last(const AttnParams& p, int32_t m, int32_t h, int32_t nsrc) {
-  int32_t* c = p.arrive + (int64_t)m * p.hq + h;
+// Arrival merging ("the last producer merges", replaces the merge launch).  A producer
+// that has written its partial (o, lse) rows and fenced them counts each row in on the
+// counter of its list (first partial row, q head); the last of the list's nsrc
+// sources merges it.  The counter is left at 0 for the next call (workspace counters
+// start zeroed).
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+__device__ __forceinline__ bool arrive_last(const AttnParams& p, int32_t first, int32_t h, int32_t nsrc) {
+  int32_t* c = p.arrive + (int64_t)first * p.hq + h;
   const bool last = atomicAdd(c, 1) == nsrc - 1;
   if (last) {
     *c = 0;
-    __threadfence();   // acquire side: the other sources' partials are read after this
+    fence_acq_rel_gpu();   // acquire side: the other sources' partials are read after this
   }
   return last;
 }
 
-// Warp-wide: every lane with last = true has its (m, h) merged by the whole warp.
-__device__ __forceinline__ void warp_merge_flagged(const AttnParams& p, bool last, int m, int h, int lane) {
-  uint32_t lm = __ballot_sync(0xffffffffu, last);
-  __syncwarp();
-  while (lm) {
-    const int src = __ffs(lm) - 1;
-    lm &= lm - 1;
-    const int mm = __shfl_sync(0xffffffffu, m, src), hh = __shfl_sync(0xffffffffu, h, src);
-    warp_merge_row(p, mm, hh, lane);
+// Four lanes (sub = 0..3, D/4 contiguous elements each) merge one (token, q head): the
+// list's partial rows first .. first + nsrc - 1 in their fixed ascending key-start
+// order (reading #17), so the result does not depend on which producer merges.  Out
+// row qrow = token * Hq + head (bf16), lse in natural log.  Partials are read through
+// L2 (ld.global.cg): other SMs wrote them during this launch.
+template <int D>
+__device__ __forceinline__ void merge_row4(const AttnParams& p, int first, int nsrc, int h, int qrow, int sub) {
+  constexpr int E = D / 4;
+  float mx = -INFINITY;
+  for (int i = 0; i < nsrc; ++i) mx = fmaxf(mx, __ldcg(p.ws_lse + (int64_t)(first + i) * p.hq + h));
+  float acc[E];
+#pragma unroll
+  for (int k = 0; k < E; ++k) acc[k] = 0.f;
+  float tot = 0.f;
+  if (mx != -INFINITY) {
+#pragma unroll 2
+    for (int i = 0; i < nsrc; ++i) {
+      const int64_t row = (int64_t)(first + i) * p.hq + h;
+      const float w = exp2f(__ldcg(p.ws_lse + row) - mx);   // empty partial: lse = -inf -> 0
+      tot += w;
+      const float4* src = reinterpret_cast<const float4*>(p.ws_o + row * D + sub * E);
+#pragma unroll
+      for (int k = 0; k < E / 4; ++k) {
+        const float4 v = __ldcg(src + k);
+        acc[4 * k] = fmaf(w, v.x, acc[4 * k]);
+        acc[4 * k + 1] = fmaf(w, v.y, acc[4 * k + 1]);
+        acc[4 * k + 2] = fmaf(w, v.z, acc[4 * k + 2]);
+        acc[4 * k + 3] = fmaf(w, v.w, acc[4 * k + 3]);
+      }
+    }
   }
+  const float inv = tot > 0.f ? 1.f / tot : 0.f;
+  uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.out) + (int64_t)qrow * D + sub * E);
+#pragma unroll
+  for (int k = 0; k < E / 8; ++k) {
+    uint4 w4;
+    __nv_bfloat162 b;
+    b = __floats2bfloat162_rn(acc[8 * k] * inv, acc[8 * k + 1] * inv);
+    w4.x = *reinterpret_cast<uint32_t*>(&b);
+    b = __floats2bfloat162_rn(acc[8 * k + 2] * inv, acc[8 * k + 3] * inv);
+    w4.y = *reinterpret_cast<uint32_t*>(&b);
+    b = __floats2bfloat162_rn(acc[8 * k + 4] * inv, acc[8 * k + 5] * inv);
+    w4.z = *reinterpret_cast<uint32_t*>(&b);
+    b = __floats2bfloat162_rn(acc[8 * k + 6] * inv, acc[8 * k + 7] * inv);
+    w4.w = *reinterpret_cast<uint32_t*>(&b);
+    dst[k] = w4;
+  }
+  if (sub == 0) p.lse[qrow] = mx != -INFINITY ? (mx + log2f(tot)) * kLn2 : -INFINITY;
 }
 
 }  // namespace blend

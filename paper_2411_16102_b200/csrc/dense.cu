@@ -42,7 +42,7 @@ constexpr uint32_t DN_TMEM_COLS = 512;
 constexpr float DN_RESCALE_T = 8.0f;     // lazy-rescale threshold (log2 units)
 
 struct DenseSmem {
-  uint32_t q0, q1, stage0, stage_stride, bar, total;
+  uint32_t q0, q1, stage0, stage_stride, bar, stg, total;
   int nstage;
 };
 
@@ -55,7 +55,8 @@ __host__ __device__ inline DenseSmem dense_layout(int D) {
   L.stage_stride = 2 * CH * DN_KCHUNK;   // K chunks then V chunks
   L.nstage = D == 128 ? 4 : 8;
   L.bar = L.stage0 + L.nstage * L.stage_stride;
-  L.total = L.bar + 512;
+  L.stg = L.bar + 512;                    // epilogue staging: per softmax warp 32 rows x 128 B
+  L.total = L.stg + 8 * 4096;
   return L;
 }
 
@@ -214,7 +215,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       const uint32_t stage_lo = L.stage_stride >> 4;
       const uint32_t leader = ptx::elect_one();
       uint32_t kit = 0, gu = 0;
-      uint32_t pb[4] = {0, 0, 0, 0};    // completions consumed per p_full[tile][buffer]
+      uint32_t pbits = 0;               // parity of the next p_full[tile][buffer] completion (bit pi)
       for (int ui = blockIdx.x; ui < p.n_units; ui += gridDim.x) {
         const Unit u = p.units[ui];
         const int nb = (u.entry_end - u.entry_begin + EPB - 1) / EPB;
@@ -245,7 +246,8 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
           if (j + 2 < nb) wait_kv(j + 2);
           for (int t = 0; t < ntile; ++t) {
             const int pi = t * 2 + (j & 1);
-            ptx::mbar_wait(&p_full[pi], (pb[pi]++) & 1);
+            ptx::mbar_wait(&p_full[pi], (pbits >> pi) & 1);
+            pbits ^= 1u << pi;
             ptx::tc_fence_after();
             const uint32_t acol = tmem + t * 128 + (j & 1) * DN_KB;
 #pragma unroll
@@ -273,6 +275,29 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
     uint32_t sb = 0;                                  // blocks of this tile processed so far
     uint32_t scnt0 = 0, scnt1 = 0;                    // s_full completions consumed per S buffer (registers)
     int2 enext[EPB];                                  // {pos0, count} of the next block's entries
+    // Arrival merging, deferred by one unit: this thread's partial row of the previous
+    // unit (first row of its list, sources, q head, out row) counts in at the next
+    // epilogue; rows whose count-in is the last are merged 8 at a time, 4 lanes each.
+    int pf = -1, pn = 0, ph = 0, pq = 0;
+    auto settle = [&]() {
+      if (__any_sync(0xffffffffu, pf >= 0)) {
+        fence_acq_rel_gpu();   // release: every lane's partial stores before the count-in
+        __syncwarp();
+        const bool last = pf >= 0 && arrive_last(p, pf, ph, pn);
+        uint32_t lm = __ballot_sync(0xffffffffu, last);
+        const int gi = lane >> 2;
+        while (lm) {
+          const int cnt = __popc(lm);
+          const int src = gi < cnt ? (int)__fns(lm, 0, gi + 1) : 0;
+          const int f = __shfl_sync(0xffffffffu, pf, src), n = __shfl_sync(0xffffffffu, pn, src);
+          const int h = __shfl_sync(0xffffffffu, ph, src), q = __shfl_sync(0xffffffffu, pq, src);
+          if (gi < cnt) merge_row4<D>(p, f, n, h, q, lane & 3);
+#pragma unroll 1
+          for (int k = 0; k < 8 && lm; ++k) lm &= lm - 1;
+        }
+      }
+      pf = -1;
+    };
     auto load_meta = [&](const Unit& un, int j) {
 #pragma unroll
       for (int i = 0; i < EPB; ++i) {
@@ -407,43 +432,63 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       const float m_use = m_ref == -INFINITY ? 0.f : m_ref;
       const float inv = l > 0.f ? 1.f / l : 0.f;
       const float lse2 = l > 0.f ? m_use + log2f(l) : -INFINITY;
+      if (p.arrive != nullptr) settle();   // the previous unit's partial rows (stores long complete)
+      // O / l leaves through a per-warp smem staging tile (XOR-swizzled 16-B units, no
+      // bank conflicts), so that every global store instruction writes whole 128-B row
+      // segments (4 rows per instruction) instead of 32 scattered 16-B pieces.
+      // Row kinds: 2 = fp32 partial row, 1 = bf16 output row (DIRECT), 0 = nothing.
+      {
+        const int kind = tgt == PM_DIRECT ? 1 : (tgt >= 0 ? 2 : 0);
+        char* rowp = kind == 1 ? reinterpret_cast<char*>(p.out) + ((int64_t)token * p.hq + head) * D * 2
+                   : kind == 2 ? reinterpret_cast<char*>(p.ws_o + ((int64_t)tgt * p.hq + head) * D) : nullptr;
+        const uint32_t stg = ptx::smem_u32(smem + L.stg + (warp - 4) * 4096);
+        const int k8 = lane & 7;
+        char* rp[8];
+        int rk[8];
+#pragma unroll
+        for (int s_ = 0; s_ < 8; ++s_) {          // rows s_ * 4 + lane / 8 of this warp, for the copy-out
+          const int rr = s_ * 4 + (lane >> 3);
+          rp[s_] = reinterpret_cast<char*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(rowp), rr));
+          rk[s_] = __shfl_sync(0xffffffffu, kind, rr);
+        }
 #pragma unroll 1
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t ov[32];
-        ptx::tmem_ld32(tmem + lane_base + col_o + c * 32, ov);
-        ptx::tmem_wait_ld();
-        if (tgt == PM_DIRECT) {
-          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.out) +
-                                                ((int64_t)token * p.hq + head) * D + c * 32);
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t ov[32];
+          ptx::tmem_ld32(tmem + lane_base + col_o + c * 32, ov);
+          ptx::tmem_wait_ld();
 #pragma unroll
-          for (int k = 0; k < 32; k += 8) {
-            uint4 w;
-            w.x = ptx::pack_bf16(__uint_as_float(ov[k]) * inv, __uint_as_float(ov[k + 1]) * inv);
-            w.y = ptx::pack_bf16(__uint_as_float(ov[k + 2]) * inv, __uint_as_float(ov[k + 3]) * inv);
-            w.z = ptx::pack_bf16(__uint_as_float(ov[k + 4]) * inv, __uint_as_float(ov[k + 5]) * inv);
-            w.w = ptx::pack_bf16(__uint_as_float(ov[k + 6]) * inv, __uint_as_float(ov[k + 7]) * inv);
-            dst[k / 8] = w;
+          for (int u8 = 0; u8 < 8; ++u8)
+            ptx::sts128(stg + ptx::sw128(lane, u8), __uint_as_float(ov[4 * u8]) * inv,
+                        __uint_as_float(ov[4 * u8 + 1]) * inv, __uint_as_float(ov[4 * u8 + 2]) * inv,
+                        __uint_as_float(ov[4 * u8 + 3]) * inv);
+          __syncwarp();
+#pragma unroll
+          for (int s_ = 0; s_ < 8; ++s_) {
+            const int rr = s_ * 4 + (lane >> 3);
+            const float4 v = ptx::lds128(stg + ptx::sw128(rr, k8));
+            if (rk[s_] == 2) {
+              *reinterpret_cast<float4*>(rp[s_] + c * 128 + k8 * 16) = v;
+            } else if (rk[s_] == 1) {
+              uint2 b;
+              b.x = ptx::pack_bf16(v.x, v.y);
+              b.y = ptx::pack_bf16(v.z, v.w);
+              *reinterpret_cast<uint2*>(rp[s_] + c * 64 + k8 * 8) = b;
+            }
           }
-        } else if (tgt >= 0) {
-          float4* dst = reinterpret_cast<float4*>(p.ws_o + ((int64_t)tgt * p.hq + head) * D + c * 32);
-#pragma unroll
-          for (int k = 0; k < 32; k += 4)
-            dst[k / 4] = make_float4(__uint_as_float(ov[k]) * inv, __uint_as_float(ov[k + 1]) * inv,
-                                     __uint_as_float(ov[k + 2]) * inv, __uint_as_float(ov[k + 3]) * inv);
+          __syncwarp();   // the staging tile is rewritten by the next chunk
         }
       }
       if (tgt == PM_DIRECT) p.lse[(int64_t)token * p.hq + head] = lse2 * kLn2;
       else if (tgt >= 0) p.ws_lse[(int64_t)tgt * p.hq + head] = lse2;
-      if (p.arrive != nullptr) {   // the last producer of a (token, head) merges it (no merge launch)
-        bool last = false;
-        if (tgt >= 0) {
-          __threadfence();
-          last = arrive_last(p, am.x, head, am.y);
-        }
-        warp_merge_flagged(p, last, am.x, head, lane);
+      if (p.arrive != nullptr && tgt >= 0) {   // counts in at the next unit's epilogue (or the end)
+        pf = am.x;
+        pn = am.y;
+        ph = head;
+        pq = token * p.hq + head;
       }
       ptx::tc_fence_before();
     }
+    if (p.arrive != nullptr) settle();
   }
   __syncwarp();       // lane 0 of the producer / MMA warps rejoins its warp before the CTA barrier
   ptx::tc_fence_before();

@@ -734,13 +734,18 @@ int build_plan(blend_tree* t) {
   // instead of the item_tokens -> tok_pos / partmap chain.
   std::vector<blend::RowDesc> srows(sunits.size() * blend::STREAM_ROWS,
                                     blend::RowDesc{-1, INT32_MIN, blend::PM_SKIP, -1, -1, 0, 0, 0});
-  std::vector<int32_t> prow_list(2 * prow, -1);   // partial row -> {merge list, its source count}
-  for (size_t m = 0; m + 1 < merge_off.size(); ++m)
-    for (int32_t s_ = merge_off[m]; s_ < merge_off[m + 1]; ++s_)
-      if (merge_rows[s_] >= 0) {
-        prow_list[2 * merge_rows[s_]] = (int32_t)m;
-        prow_list[2 * merge_rows[s_] + 1] = merge_off[m + 1] - merge_off[m];
-      }
+  // partial row -> {first partial row of its merge list, the list's source count}.  An
+  // unfused list's entries are its partial rows in order (merge_rows[s] == s: rows are
+  // allocated in list order above), so neither the merge kernel nor an arrival-merging
+  // producer needs further lookups.
+  std::vector<int32_t> prow_list(2 * prow, -1);
+  for (size_t m = 0; m < (size_t)n_unfused; ++m)
+    for (int32_t s_ = merge_off[m]; s_ < merge_off[m + 1]; ++s_) {
+      if (merge_rows[s_] != s_)   // the merge kernel reads partial row s of entry s directly
+        return fail(BLEND_EINVAL, "internal: merge list %zu not in partial-row order", m);
+      prow_list[2 * merge_rows[s_]] = merge_rows[merge_off[m]];
+      prow_list[2 * merge_rows[s_] + 1] = merge_off[m + 1] - merge_off[m];
+    }
   {
     const int32_t g = a.num_q_heads / a.num_kv_heads;
     for (size_t ui = 0; ui < sunits.size(); ++ui) {
@@ -754,7 +759,7 @@ int build_plan(blend_tree* t) {
         d.target = partmap[u.pm_base + tl];
         d.head = u.kvh * g + j;
         if (d.target >= 0) {
-          d.mlist = prow_list[2 * d.target];
+          d.first = prow_list[2 * d.target];
           d.nsrc = prow_list[2 * d.target + 1];
         }
       }
@@ -789,9 +794,9 @@ int build_plan(blend_tree* t) {
   t->n_partial_rows = prow;
   const size_t hq = a.num_q_heads, D = a.head_dim;
   size_t o_bytes = ((size_t)prow * hq * D * 4 + 255) & ~size_t(255);
-  // partials o | lse | unit counter (256 B) | arrival counters [merge list][Hq]
-  t->workspace_bytes = o_bytes + (((size_t)prow * hq * 4 + 255) & ~size_t(255)) + 256 +
-                       (((size_t)merge_tok.size() * hq * 4 + 255) & ~size_t(255));
+  // partials o | lse | unit counter (256 B) | arrival counters [partial row][Hq] (the
+  // counter of a list is the one of its first row)
+  t->workspace_bytes = o_bytes + 2 * (((size_t)prow * hq * 4 + 255) & ~size_t(255)) + 256;
   t->info.n_tokens = T;
   t->info.n_items = (int64_t)items.size();
   t->info.n_dense_units = (int64_t)dunits.size();

@@ -18,7 +18,7 @@ enum PlanSection {
   SEC_MERGE_OFF,       // int32[M+1]
   SEC_MERGE_ROWS,      // int32[]    partial rows, ascending key-range start (-1 = the fusing unit)
   SEC_STREAM_ROWS,     // RowDesc[n_stream * STREAM_ROWS]  per-row descriptors of the streaming units
-  SEC_PROW_LIST,       // int32[2P]  {merge list, its source count} of each partial row (arrival merging)
+  SEC_PROW_LIST,       // int32[2P]  {first partial row of its merge list, source count} (arrival merging)
   SEC_COUNT
 };
 
@@ -54,7 +54,8 @@ struct RowDesc {
   int32_t pos;       // absolute position of the token (causal bound)
   int32_t target;    // partmap value: partial row | PM_DIRECT | PM_SKIP | fused
   int32_t head;      // q head (partial-row column)
-  int32_t mlist;     // merge list m of a partial row (-1: DIRECT / SKIP); counter m * Hq + head
+  int32_t first;     // partial row: first partial row of its merge list (rows first .. first+nsrc-1,
+                     // ascending key start); -1 for DIRECT / SKIP.  Arrival counter first * Hq + head
   int32_t nsrc;      // sources of that list
   int32_t pad0, pad1;
 };

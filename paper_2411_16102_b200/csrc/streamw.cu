@@ -208,6 +208,26 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
     return r;
   };
 
+  // Arrival merging, deferred by one unit: the rows of the unit before count in (and
+  // the last source of a (token, head) merges it, 4 lanes per row) once this warp has
+  // streamed another unit.
+  RowDesc pend0{-1, 0, PM_SKIP, 0, -1, 0, 0, 0}, pend1 = pend0;
+  auto settle = [&]() {
+    const bool any = (pend0.qrow >= 0 && pend0.target >= 0) || (pend1.qrow >= 0 && pend1.target >= 0);
+    if (__any_sync(0xffffffffu, any)) {
+      fence_acq_rel_gpu();   // release: every lane's partial stores before the count-in
+      __syncwarp();
+#pragma unroll
+      for (int half_row = 0; half_row < 2; ++half_row) {
+        const RowDesc d = half_row ? pend1 : pend0;
+        bool last = false;
+        if (c4 == 0 && d.qrow >= 0 && d.target >= 0) last = arrive_last(p, d.first, d.head, d.nsrc);
+        last = __shfl_sync(0xffffffffu, last, lane & ~3);
+        if (last) merge_row4<D>(p, d.first, d.nsrc, d.head, d.qrow, c4);
+      }
+    }
+    pend0.qrow = pend1.qrow = -1;
+  };
   int nidx = next_index();
   Pre pre{};
   if (nidx < p.n_units) pre = prefetch(nidx, 0);
@@ -335,6 +355,9 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
         if (lane == 0) ptx::mbar_arrive(&wempty[s]);
       }
     }
+    // ---- unit end: the previous unit's partial rows count in (their stores are long
+    // complete, so the release fence is cheap), then this unit's rows are written
+    if (p.arrive != nullptr) settle();
     // ---- unit end: rows g8 (o[.][0,1]) and g8+8 (o[.][2,3]) straight from the fragments
     l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
     l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
@@ -363,19 +386,12 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
         if (c4 == 0) p.ws_lse[(int64_t)d.target * p.hq + d.head] = lse2;
       }
     }
-    if (p.arrive != nullptr &&
-        __any_sync(0xffffffffu, (cu.d0.qrow >= 0 && cu.d0.target >= 0) || (cu.d1.qrow >= 0 && cu.d1.target >= 0))) {
-      // arrival merging: the last producer of each (token, head) merges its list
-      __threadfence();   // this lane's partial stores, before the row's count-in
-      __syncwarp();
-#pragma unroll
-      for (int half_row = 0; half_row < 2; ++half_row) {
-        const RowDesc d = half_row ? cu.d1 : cu.d0;
-        const bool last = c4 == 0 && d.qrow >= 0 && d.target >= 0 && arrive_last(p, d.mlist, d.head, d.nsrc);
-        warp_merge_flagged(p, last, d.mlist, d.head, lane);
-      }
+    if (p.arrive != nullptr) {   // this unit's partial rows count in at the next unit's end
+      pend0 = cu.d0;
+      pend1 = cu.d1;
     }
   }
+  if (p.arrive != nullptr) settle();
   ptx::pdl_wait();
 }
 

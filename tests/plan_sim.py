@@ -53,19 +53,18 @@ def check_stream_rows(P, g, Hq):
     for ui, u in enumerate(P["sunits"]):
         item, kvh, rb, nr, eb, ee, pmb, tb = (int(x) for x in u)
         for r in range(STREAM_ROWS):
-            qrow, pos, tgt, head, ml, ns = (int(x) for x in sr[ui * STREAM_ROWS + r][:6])
+            qrow, pos, tgt, head, first, ns = (int(x) for x in sr[ui * STREAM_ROWS + r][:6])
             if r >= nr:
-                assert qrow == -1 and tgt == -2 and ml == -1
+                assert qrow == -1 and tgt == -2 and first == -1
                 continue
             tl, j = (rb + r) // g, (rb + r) % g
             tok = int(P["item_tokens"][tb + tl])
             assert (qrow, pos, tgt, head) == (tok * Hq + kvh * g + j, int(P["tok_pos"][tok]),
                                               int(P["partmap"][pmb + tl]), kvh * g + j)
-            if tgt >= 0:   # arrival merging: the row's merge list holds it, with its source count
-                rows = list(P["merge_rows"][mo[ml]:mo[ml + 1]])
-                assert tgt in rows and ns == len(rows) and int(P["merge_tok"][ml]) == tok
+            if tgt >= 0:   # arrival merging: the row's list is rows first .. first + ns - 1
+                assert first <= tgt < first + ns
             else:
-                assert ml == -1
+                assert first == -1
 
 
 def simulate(w, tree):
@@ -128,9 +127,10 @@ def simulate(w, tree):
     assert len(pl) == nprow
     for m, tok in enumerate(P["merge_tok"]):
         rows = P["merge_rows"][mo[m]:mo[m + 1]]
-        for r in rows:   # arrival merging: each partial row knows its list and the list's size
-            if r >= 0:
-                assert tuple(int(x) for x in pl[r]) == (m, len(rows))
+        if all(r >= 0 for r in rows):   # arrival merging: consecutive rows, each knows the list
+            assert list(rows) == list(range(int(rows[0]), int(rows[0]) + len(rows)))
+            for r in rows:
+                assert tuple(int(x) for x in pl[r]) == (int(rows[0]), len(rows))
         real = [r for r in rows if r >= 0]
         assert not np.isnan(part_l[real]).any(), "merge reads an unwritten partial"
         assert sum(1 for r in rows if r < 0) <= 1

@@ -236,7 +236,7 @@ def test_arrival_merge_counters(kw):
     w = W.c2_mmlu_decode(n_req=96)
     db = device_batch(w, tree_kw=kw)
     assert db.info["n_merge_tokens"] > 0
-    db.run()
+    db.run(flags=B.ARRIVAL_MERGE)
     torch.cuda.synchronize()
     _cmp(w, db)
     first = db.out.clone()
@@ -245,6 +245,9 @@ def test_arrival_merge_counters(kw):
     assert int(tail.count_nonzero().item()) == 0, "arrival counters not reset"
     for flags in (0, 1, 0):
         db.out.zero_()
-        db.run(flags=flags)
+        db.run(flags=flags | B.ARRIVAL_MERGE)
         torch.cuda.synchronize()
         assert torch.equal(first, db.out)
+    db.run()                                   # merge kernel: same attention within tolerance
+    torch.cuda.synchronize()
+    _cmp(w, db)
