@@ -105,6 +105,8 @@ extern "C" int blend_attention(const blend_attn_args* a, void* stream) {
   p.merge_rows = (const int32_t*)(base + pl.off[SEC_MERGE_ROWS]);
   p.srows = (const RowDesc*)(base + pl.off[SEC_STREAM_ROWS]);
   p.prow_list = (const int32_t*)(base + pl.off[SEC_PROW_LIST]);
+  p.dqtok = (const int32_t*)(base + pl.off[SEC_DENSE_QTOK]);
+  p.n_tokens = (int32_t)pl.count[SEC_TOK_POS];
   p.n_merge = (int32_t)pl.count[SEC_MERGE_TOK];
   p.hq = hq;
   p.hkv = pl.num_kv_heads;

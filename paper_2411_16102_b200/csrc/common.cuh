@@ -37,7 +37,9 @@ struct AttnParams {
   const RowDesc* srows;  // streaming units' row descriptors (SEC_STREAM_ROWS)
   int32_t* sched;        // workspace word: dynamic unit counter of the streaming pass (zeroed per call)
   const int32_t* prow_list;   // partial row -> {merge list, source count} (SEC_PROW_LIST)
-  int32_t* arrive;       // arrival counters [merge list][Hq] (workspace; NULL: the merge kernel merges)
+  int32_t* arrive;       // arrival counters [partial row][Hq] (workspace; NULL: the merge kernel merges)
+  const int32_t* dqtok;  // dense units: first token when the unit's tokens are consecutive, else -1
+  int32_t n_tokens;      // query tokens (rows of q / out)
 };
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {

@@ -27,6 +27,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <math.h>
+#include <string.h>
 
 #include "blend.h"
 #include "common.cuh"
@@ -62,7 +63,8 @@ __host__ __device__ inline DenseSmem dense_layout(int D) {
 
 template <int D, int BOX>
 __global__ void __launch_bounds__(DN_THREADS, 1)
-    dense_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv, AttnParams p) {
+    dense_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
+                 const __grid_constant__ CUtensorMap tmq, AttnParams p) {
   constexpr int CH = D / 64;
   constexpr int EPB = DN_KB / BOX;      // page entries per 64-key block
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -167,11 +169,29 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
     }
   } else if (warp == 3) {
     // ===================== Q loader: next unit's rows as soon as its last QK is issued =====
+    // A unit whose tokens are consecutive rows of q (a prefill chunk) loads each 128-row
+    // tile chunk with one 3-D TMA box {64 cols, g heads, 128/g tokens}; other units (a
+    // SEPARATE node's tokens come from many requests) gather rows with cp.async.
+    if (lane == 0 && 128 % p.g == 0) ptx::tma_prefetch_desc(&tmq);
     uint32_t gu = 0;
     for (int ui = blockIdx.x; ui < p.n_units; ui += gridDim.x, ++gu) {
       const Unit u = p.units[ui];
+      const int qt0 = p.dqtok[ui];
       if (gu > 0) ptx::mbar_wait(q_empty, (gu - 1) & 1);
       const int nrows = u.n_rows > 128 ? 256 : 128;
+      if (qt0 >= 0) {
+        if (lane == 0) {
+          const int ntile = nrows >> 7;
+          ptx::mbar_arrive_expect_tx(q_full, (uint32_t)(ntile * CH * DN_QCHUNK));
+          for (int t = 0; t < ntile; ++t)
+#pragma unroll
+            for (int c = 0; c < CH; ++c)
+              ptx::tma_load_3d(smem + (t ? L.q1 : L.q0) + c * DN_QCHUNK, &tmq, q_full, c * 64, u.kvh * p.g,
+                               qt0 + t * (128 / p.g));
+        }
+        __syncwarp();
+        continue;
+      }
       for (int row = lane; row < nrows; row += 32) {
         uint8_t* qs = smem + ((row >> 7) ? L.q1 : L.q0);
         const int r = row & 127;
@@ -500,6 +520,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
 }
 
 cudaError_t make_cache_tmap(CUtensorMap* m, const void* base, int64_t rows, int D, int box_rows);
+cudaError_t make_q_tmap(CUtensorMap* m, const void* base, int64_t T, int hq, int D, int g);
 cudaError_t set_smem_once(const void* func, size_t bytes);
 int num_sms_cached();
 
@@ -511,11 +532,17 @@ static cudaError_t launch_dense_db(const AttnParams& p, int64_t n_cache_pages, c
   if (e != cudaSuccess) return e;
   e = make_cache_tmap(&tv, p.v_cache, rows, D, BOX);
   if (e != cudaSuccess) return e;
+  CUtensorMap tq;   // only dereferenced for units the planner marked (128 % g == 0)
+  memset(&tq, 0, sizeof(tq));
+  if (128 % p.g == 0) {
+    e = make_q_tmap(&tq, p.q, p.n_tokens, p.hq, D, p.g);
+    if (e != cudaSuccess) return e;
+  }
   const size_t smem = dense_layout(D).total + 1024;
   e = set_smem_once((const void*)dense_kernel<D, BOX>, smem);
   if (e != cudaSuccess) return e;
   const int grid = p.n_units < num_sms_cached() ? p.n_units : num_sms_cached();
-  dense_kernel<D, BOX><<<grid, DN_THREADS, smem, st>>>(tk, tv, p);
+  dense_kernel<D, BOX><<<grid, DN_THREADS, smem, st>>>(tk, tv, tq, p);
   return cudaPeekAtLastError();
 }
 

@@ -729,6 +729,20 @@ int build_plan(blend_tree* t) {
   for (size_t ii = 0; ii < items.size(); ++ii)
     std::copy(items[ii].toks.begin(), items[ii].toks.end(), item_tokens.begin() + item_tok_off[ii]);
 
+  // Dense units whose query tokens are consecutive rows of q (a request's prefill chunk)
+  // and whose 128-row tiles hold whole tokens load Q with 3-D TMA boxes {64, g, 128/g}.
+  std::vector<int32_t> dqtok(dunits.size(), -1);
+  if (blend::DENSE_ROWS % g == 0 && 128 % g == 0)
+    for (size_t ui = 0; ui < dunits.size(); ++ui) {
+      const blend::Unit& u = dunits[ui];
+      const int32_t tl0 = u.row_begin / g, tl1 = (u.row_begin + u.n_rows - 1) / g;
+      if (u.row_begin % g) continue;
+      const int32_t t0 = item_tokens[u.tok_base + tl0];
+      bool consec = true;
+      for (int32_t tl = tl0 + 1; tl <= tl1 && consec; ++tl) consec = item_tokens[u.tok_base + tl] == t0 + (tl - tl0);
+      if (consec) dqtok[ui] = t0;
+    }
+
   // Per-row descriptors of the streaming units (STREAM_ROWS slots per unit): the
   // kernel gets each row's q/out row, position and partmap target in one load
   // instead of the item_tokens -> tok_pos / partmap chain.
@@ -789,6 +803,7 @@ int build_plan(blend_tree* t) {
   put(SEC_MERGE_ROWS, merge_rows.data(), 4, merge_rows.size());
   put(SEC_STREAM_ROWS, srows.data(), sizeof(RowDesc), srows.size());
   put(SEC_PROW_LIST, prow_list.data(), 4, prow_list.size());
+  put(SEC_DENSE_QTOK, dqtok.data(), 4, dqtok.size());
   blob.resize((blob.size() + 255) & ~size_t(255));
 
   t->n_partial_rows = prow;

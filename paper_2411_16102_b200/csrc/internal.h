@@ -19,6 +19,8 @@ enum PlanSection {
   SEC_MERGE_ROWS,      // int32[]    partial rows, ascending key-range start (-1 = the fusing unit)
   SEC_STREAM_ROWS,     // RowDesc[n_stream * STREAM_ROWS]  per-row descriptors of the streaming units
   SEC_PROW_LIST,       // int32[2P]  {first partial row of its merge list, source count} (arrival merging)
+  SEC_DENSE_QTOK,      // int32[n_dense]  first token of a dense unit whose tokens are consecutive
+                       //                 (its Q tiles load by TMA boxes), else -1
   SEC_COUNT
 };
 

@@ -414,6 +414,45 @@ static cudaError_t encode_cache_tmap(CUtensorMap* m, const void* base, int64_t r
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// 3-D view of q [T][Hq][D] bf16, box {64 cols, g heads, 128/g tokens} (one 128-row
+// dense Q tile chunk), 128B swizzle.  Cached like the cache maps.
+namespace {
+struct QmapEntry {
+  const void* base;
+  int64_t T;
+  int hq, D, g;
+  CUtensorMap map;
+};
+QmapEntry g_qmaps[8];
+int g_qmap_n = 0, g_qmap_next = 0;
+}  // namespace
+
+cudaError_t make_q_tmap(CUtensorMap* m, const void* base, int64_t T, int hq, int D, int g) {
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  for (int i = 0; i < g_qmap_n; ++i) {
+    const QmapEntry& t = g_qmaps[i];
+    if (t.base == base && t.T == T && t.hq == hq && t.D == D && t.g == g) {
+      *m = t.map;
+      return cudaSuccess;
+    }
+  }
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return cudaErrorNotSupported;
+  cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)hq, (cuuint64_t)(T > 0 ? T : 1)};
+  cuuint64_t strides[2] = {(cuuint64_t)D * 2, (cuuint64_t)hq * D * 2};
+  cuuint32_t box[3] = {64, (cuuint32_t)g, (cuuint32_t)(128 / g)};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  QmapEntry& t = g_qmaps[g_qmap_next];
+  t = {base, T, hq, D, g, *m};
+  g_qmap_next = (g_qmap_next + 1) % 8;
+  if (g_qmap_n < 8) ++g_qmap_n;
+  return cudaSuccess;
+}
+
 int num_sms_cached() {
   static int n = 0;
   if (!n) {

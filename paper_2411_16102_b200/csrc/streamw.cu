@@ -45,7 +45,7 @@ __host__ __device__ inline StreamWSmem streamw_layout(int D) {
   L.q_stride = 2 * CH * 2048;
   L.bar = L.q0 + SW_WARPS * L.q_stride;
   L.uq = L.bar + 2 * SW_WARPS * SW_STAGES * 8 + 2 * SW_WARPS * 2 * 8;   // + unit-queue barriers
-  L.total = L.uq + SW_WARPS * 2 * 4;
+  L.total = L.uq + SW_WARPS * 2 * 16;
   return L;
 }
 
@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
   uint64_t* empty = full + SW_WARPS * SW_STAGES;
   uint64_t* uqf = empty + SW_WARPS * SW_STAGES;   // [ring][2] unit index announced
   uint64_t* uqe = uqf + SW_WARPS * 2;             // [ring][2] announcement consumed
-  int32_t* uq = reinterpret_cast<int32_t*>(smem + L.uq);   // [ring][2] unit index (>= n_units: done)
+  int4* uq = reinterpret_cast<int4*>(smem + L.uq);   // [ring][2] {unit (>= n_units: done), entry begin, count}
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   ptx::pdl_launch_dependents();
 
@@ -93,64 +93,70 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
       uint64_t* rempty = empty + w * SW_STAGES;
       uint8_t* ring = smem + L.ring0 + w * L.ring_stride;
       uint32_t a = 0, it = 0;
-      auto announce = [&](int idx) {
+      // announcements carry {unit, first entry, entry count}: the consumer prefetches the
+      // unit's rows and entries without a dependent global load
+      auto announce = [&](int idx, const Unit& u) {
         const uint32_t s = a & 1, ph = (a >> 1) & 1;
         ptx::mbar_wait(&uqe[w * 2 + s], ph ^ 1);
-        uq[w * 2 + s] = idx;
+        uq[w * 2 + s] = make_int4(idx, u.entry_begin, u.entry_end - u.entry_begin, 0);
         ptx::mbar_arrive(&uqf[w * 2 + s]);   // release: the consumer reads the slot after its wait
         ++a;
       };
-      int idx = atomicAdd(p.sched, 1);
-      announce(idx);
-      if (idx < p.n_units) {
-        Unit un = p.units[idx];
-        int nidx = atomicAdd(p.sched, 1);   // consumed one unit later
-        int4 cur = ents[un.entry_begin];
-        while (true) {
-          Unit nun{};
-          int4 nfirst = make_int4(0, 0, 0, 0);
-          int phase = 0;   // 1: next unit announced and its Unit requested, 2: its first entry requested
-          for (int e = un.entry_begin; e < un.entry_end; ++e) {
-            const int4 nxt = e + 1 < un.entry_end ? ents[e + 1] : make_int4(0, 0, 0, 0);
-            const int count = cur.w;
-            for (int h = 0; h * SW_KEYS < count; ++h, ++it) {
-              const uint32_t s = it % SW_STAGES, ph = (it / SW_STAGES) & 1;
-              ptx::mbar_wait(&rempty[s], ph ^ 1);
-              const int left = count - h * SW_KEYS;
-              const int rows = ((left < SW_KEYS ? left : SW_KEYS) + 15) & ~15;
-              const int32_t y = (cur.x * p.hkv + un.kvh) * p.ps + cur.y + h * SW_KEYS;
-              uint8_t* st = ring + s * L.stage_stride;
-              ptx::mbar_arrive_expect_tx(&rfull[s], 2u * CH * rows * 128u);
+      const int n = p.n_units;
+      // Unit pipeline, two deep: while unit k's stages are issued, unit k+1 is known
+      // (struct loaded, announced, first entry requested) and unit k+2's index is being
+      // fetched from the counter, so no dependent global load sits between two units.
+      int i_cur = atomicAdd(p.sched, 1);
+      int i_nxt = atomicAdd(p.sched, 1);
+      Unit u_cur = i_cur < n ? p.units[i_cur] : Unit{};
+      announce(i_cur, u_cur);
+      int4 cur = i_cur < n ? ents[u_cur.entry_begin] : make_int4(0, 0, 0, 0);
+      while (i_cur < n) {
+        Unit u_nxt{};
+        int4 nfirst = make_int4(0, 0, 0, 0);
+        int i_nn = n;
+        if (i_nxt < n) u_nxt = p.units[i_nxt];   // requested now, used after the first stage's issue
+        int phase = 1;   // 2: next unit announced, its first entry and the index after it requested
+        auto advance = [&]() {
+          if (phase == 1) {
+            announce(i_nxt, u_nxt);
+            if (i_nxt < n) {
+              nfirst = ents[u_nxt.entry_begin];
+              i_nn = atomicAdd(p.sched, 1);
+            }
+            phase = 2;
+          }
+        };
+        for (int e = u_cur.entry_begin; e < u_cur.entry_end; ++e) {
+          const int4 nxt = e + 1 < u_cur.entry_end ? ents[e + 1] : make_int4(0, 0, 0, 0);
+          const int count = cur.w;
+          for (int h = 0; h * SW_KEYS < count; ++h, ++it) {
+            const uint32_t s = it % SW_STAGES, ph = (it / SW_STAGES) & 1;
+            ptx::mbar_wait(&rempty[s], ph ^ 1);
+            const int left = count - h * SW_KEYS;
+            const int rows = ((left < SW_KEYS ? left : SW_KEYS) + 15) & ~15;
+            const int32_t y = (cur.x * p.hkv + u_cur.kvh) * p.ps + cur.y + h * SW_KEYS;
+            uint8_t* st = ring + s * L.stage_stride;
+            ptx::mbar_arrive_expect_tx(&rfull[s], 2u * CH * rows * 128u);
 #pragma unroll
-              for (int c = 0; c < CH; ++c) {
-                if (rows == SW_KEYS) {
-                  ptx::tma_load_2d(st + c * SW_CHUNK, &tmk32, &rfull[s], c * 64, y);
-                  ptx::tma_load_2d(st + (CH + c) * SW_CHUNK, &tmv32, &rfull[s], c * 64, y);
-                } else {
-                  ptx::tma_load_2d(st + c * SW_CHUNK, &tmk16, &rfull[s], c * 64, y);
-                  ptx::tma_load_2d(st + (CH + c) * SW_CHUNK, &tmv16, &rfull[s], c * 64, y);
-                }
-              }
-              // the unit's first loads are in flight: hand out the next unit, then fetch its
-              // metadata one stage later, so no dependent load sits right before a TMA issue
-              if (phase == 1 && nidx < p.n_units) {
-                nfirst = ents[nun.entry_begin];
-                phase = 2;
-              }
-              if (phase == 0) {
-                announce(nidx);
-                if (nidx < p.n_units) nun = p.units[nidx];
-                phase = 1;
+            for (int c = 0; c < CH; ++c) {
+              if (rows == SW_KEYS) {
+                ptx::tma_load_2d(st + c * SW_CHUNK, &tmk32, &rfull[s], c * 64, y);
+                ptx::tma_load_2d(st + (CH + c) * SW_CHUNK, &tmv32, &rfull[s], c * 64, y);
+              } else {
+                ptx::tma_load_2d(st + c * SW_CHUNK, &tmk16, &rfull[s], c * 64, y);
+                ptx::tma_load_2d(st + (CH + c) * SW_CHUNK, &tmv16, &rfull[s], c * 64, y);
               }
             }
-            cur = nxt;
+            advance();   // one pipeline step per issued stage, after its loads are in flight
           }
-          if (nidx >= p.n_units) break;
-          if (phase == 1) nfirst = ents[nun.entry_begin];
-          un = nun;
-          cur = nfirst;
-          nidx = atomicAdd(p.sched, 1);
+          cur = nxt;
         }
+        advance();
+        i_cur = i_nxt;
+        u_cur = u_nxt;
+        cur = nfirst;
+        i_nxt = i_nn;
       }
     }
     ptx::pdl_wait();   // this grid completes only after the (overlapped) dense grid has completed
@@ -171,14 +177,14 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
   constexpr int CPL = (16 * D / 8) / 32;   // 16-byte Q chunks per lane (row = lane / 2)
 
   uint32_t a = 0;
-  auto next_index = [&]() -> int {   // the ring's next announced unit (>= n_units: no more work)
+  auto next_index = [&]() -> int4 {   // the ring's next announced unit (x >= n_units: no more work)
     const uint32_t s = a & 1, ph = (a >> 1) & 1;
     ptx::mbar_wait(&uqf[warp * 2 + s], ph);
-    const int idx = uq[warp * 2 + s];
+    const int4 ann = uq[warp * 2 + s];
     __syncwarp();
     if (lane == 0) ptx::mbar_arrive(&uqe[warp * 2 + s]);
     ++a;
-    return idx;
+    return ann;
   };
   struct Pre {
     RowDesc d0, d1;        // rows g8 and g8 + 8 (softmax / output rows of this lane)
@@ -186,15 +192,14 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
     int4 ebatch;           // entry eb + lane (lane < ne)
   };
   // issue every load of unit idx; Q goes to buffer buf by cp.async
-  auto prefetch = [&](int idx, int buf) -> Pre {
+  auto prefetch = [&](const int4 ann, int buf) -> Pre {
     Pre r;
-    const RowDesc* rd = p.srows + (int64_t)idx * STREAM_ROWS;
+    const RowDesc* rd = p.srows + (int64_t)ann.x * STREAM_ROWS;
     const RowDesc dq = rd[lane >> 1];
     r.d0 = rd[g8];
     r.d1 = rd[g8 + 8];
-    const int2 er = *reinterpret_cast<const int2*>(&p.units[idx].entry_begin);
-    r.eb = er.x;
-    r.ne = er.y - er.x;
+    r.eb = ann.y;
+    r.ne = ann.z;
     r.ebatch = lane < r.ne ? ents[r.eb + lane] : make_int4(0, 0, 0, 0);
     const bool valid = dq.qrow >= 0;
     const __nv_bfloat16* src = reinterpret_cast<const __nv_bfloat16*>(p.q) + (valid ? (int64_t)dq.qrow * D : 0);
@@ -228,10 +233,10 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
     }
     pend0.qrow = pend1.qrow = -1;
   };
-  int nidx = next_index();
+  int4 nann = next_index();
   Pre pre{};
-  if (nidx < p.n_units) pre = prefetch(nidx, 0);
-  for (int buf = 0; nidx < p.n_units; buf ^= 1) {
+  if (nann.x < p.n_units) pre = prefetch(nann, 0);
+  for (int buf = 0; nann.x < p.n_units; buf ^= 1) {
     const Pre cu = pre;
     ptx::cp_async_wait_group0();
     __syncwarp();
@@ -245,8 +250,8 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
                    qa[kk][1], qa[kk][2], qa[kk][3]);
     }
     __syncwarp();   // every lane's ldmatrix of this buffer is done before the next prefetch targets it later
-    nidx = next_index();
-    if (nidx < p.n_units) pre = prefetch(nidx, buf ^ 1);
+    nann = next_index();
+    if (nann.x < p.n_units) pre = prefetch(nann, buf ^ 1);
     const int32_t pos0r = cu.d0.qrow >= 0 ? cu.d0.pos : INT32_MIN;
     const int32_t pos1r = cu.d1.qrow >= 0 ? cu.d1.pos : INT32_MIN;
 

@@ -16,7 +16,7 @@ from oracle import attention as A
 from synth import values as V
 
 SEC = ["tok_pos", "item_tok_off", "item_tokens", "entries", "dunits", "sunits", "partmap",
-       "merge_tok", "merge_off", "merge_rows", "stream_rows", "prow_list"]
+       "merge_tok", "merge_off", "merge_rows", "stream_rows", "prow_list", "dense_qtok"]
 
 
 def plan_image(tree):
@@ -67,6 +67,22 @@ def check_stream_rows(P, g, Hq):
                 assert first == -1
 
 
+def check_dense_qtok(P, g):
+    """A dense unit marked for TMA Q loading (first token t0 >= 0) covers whole tokens
+    t0, t0+1, ... of q; every unit with consecutive whole tokens is marked when its
+    128-row tiles hold whole tokens."""
+    qt = P["dense_qtok"]
+    assert len(qt) == len(P["dunits"])
+    for ui, u in enumerate(P["dunits"]):
+        item, kvh, rb, nr, eb, ee, pmb, tb = (int(x) for x in u)
+        toks = [int(P["item_tokens"][tb + tl]) for tl in range(rb // g, (rb + nr - 1) // g + 1)]
+        consec = rb % g == 0 and toks == list(range(toks[0], toks[0] + len(toks)))
+        if 256 % g == 0 and 128 % g == 0:
+            assert int(qt[ui]) == (toks[0] if consec else -1), (ui, int(qt[ui]), toks[:4])
+        else:
+            assert int(qt[ui]) == -1
+
+
 def simulate(w, tree):
     view = tree.view()
     P = plan_image(tree)
@@ -88,6 +104,7 @@ def simulate(w, tree):
     fused = {}
     dense_rows = set()
     check_stream_rows(P, g, Hq)
+    check_dense_qtok(P, g)
     for kind, units in (("dense", P["dunits"]), ("stream", P["sunits"])):
         for u in units:
             item, kvh, rb, nr, eb, ee, pmb, tb = (int(x) for x in u)
