@@ -23,6 +23,12 @@ cudaError_t launch_streamw(const AttnParams& p, int64_t n_cache_pages, cudaStrea
 cudaError_t launch_dense(const AttnParams& p, int64_t n_cache_pages, cudaStream_t st);
 }  // namespace blend
 
+static unsigned long long* g_trace = nullptr;   // diagnostics: dense-kernel timeline stamps
+extern "C" int blend_internal_set_trace(void* dev) {
+  g_trace = (unsigned long long*)dev;
+  return 0;
+}
+
 namespace {
 int cuda_fail(cudaError_t e) { return blend_internal_fail(BLEND_ECUDA, cudaGetErrorString(e)); }
 
@@ -140,6 +146,7 @@ extern "C" int blend_attention(const blend_attn_args* a, void* stream) {
                        (pd.n_units == 0 || a->path != BLEND_PATH_NO_TCGEN05);
   int32_t* arrive = arrival ? (int32_t*)((char*)a->workspace + o_bytes + lse_bytes + 256) : nullptr;
   pd.arrive = arrive;
+  pd.trace = g_trace;
   pd.sched = stream_dyn && dense_tc ? p.sched : nullptr;
   if (stream_dyn && !dense_tc) {
     e = cudaMemsetAsync(p.sched, 0, sizeof(int32_t), st);

@@ -40,7 +40,17 @@ struct AttnParams {
   int32_t* arrive;       // arrival counters [partial row][Hq] (workspace; NULL: the merge kernel merges)
   const int32_t* dqtok;  // dense units: first token when the unit's tokens are consecutive, else -1
   int32_t n_tokens;      // query tokens (rows of q / out)
+  unsigned long long* trace;   // diagnostics only (blend_internal_set_trace): [CTA][64] globaltimer stamps
 };
+
+// Diagnostics: stamp slot k of this CTA's trace row (no-op unless a trace buffer is set).
+__device__ __forceinline__ void trace_stamp(const AttnParams& p, int k) {
+  if (p.trace != nullptr && k < 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[(size_t)blockIdx.x * 64 + k] = t;
+  }
+}
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z += 0x9E3779B97F4A7C15ull;

@@ -82,6 +82,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 30);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) trace_stamp(p, 0);
   if (p.sched != nullptr && blockIdx.x == 0) {
     // reset the streaming pass's unit counter before this CTA's launch trigger: the
     // dependent (streaming) grid cannot start before every CTA of this grid has triggered
@@ -111,6 +112,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) trace_stamp(p, 1);
   // TMEM columns: S[tile][buffer] 64 fp32 columns each at tile*128 + buffer*64 (P, bf16
   // pairs, aliases the first 32 columns of its S buffer); O[tile] at 256 + tile*D.
   // register budget: warpgroup 0 (producer, MMA, allocator, Q loader) needs few; the
@@ -150,6 +152,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
           ptx::mbar_wait(&kv_empty[s], ph ^ 1);
           uint8_t* kst = smem + L.stage0 + s * L.stage_stride;
           uint8_t* vst = kst + CH * DN_KCHUNK;
+          if (kit == 0) trace_stamp(p, 3);
           ptx::mbar_arrive_expect_tx(&kv_full[s], 2u * CH * DN_KCHUNK);
 #pragma unroll
           for (int i = 0; i < EPB; ++i) {
@@ -256,6 +259,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         };
         ptx::mbar_wait(q_full, gu & 1);
         ptx::tc_fence_after();
+        if (gu == 0 && lane == 0) trace_stamp(p, 2);
         for (int j = 0; j < 2 && j < nb; ++j) {
           wait_kv(j);
           for (int t = 0; t < ntile; ++t) issue_qk(t, j);
@@ -366,6 +370,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         }
         ptx::mbar_wait(&s_full[t * 2 + buf], (buf ? scnt1++ : scnt0++) & 1);   // per-buffer completion count
         ptx::tc_fence_after();
+        if (threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 8 + 2 * j);
         float sv[DN_KB];
         ptx::tmem_ld32(tmem + lane_base + col_s, reinterpret_cast<uint32_t*>(sv));
         ptx::tmem_ld32(tmem + lane_base + col_s + 32, reinterpret_cast<uint32_t*>(sv + 32));
@@ -441,7 +446,9 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&p_full[t * 2 + buf]);
+        if (threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 9 + 2 * j);
       }
+      if (threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 4);
       // ---- epilogue: PV of the unit's last block done (MMAs complete in issue order, so
       // this also certifies every earlier PV of the unit)
       {
@@ -507,12 +514,14 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         pq = token * p.hq + head;
       }
       ptx::tc_fence_before();
+      if (threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 5);
     }
     if (p.arrive != nullptr) settle();
   }
   __syncwarp();       // lane 0 of the producer / MMA warps rejoins its warp before the CTA barrier
   ptx::tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) trace_stamp(p, 6);
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, DN_TMEM_COLS);
