@@ -61,10 +61,12 @@ __host__ __device__ inline DenseSmem dense_layout(int D) {
   return L;
 }
 
-template <int D, int BOX>
+// POLY: bit k set -> pair k (of 16 per 32-key chunk) takes the FMA-pipe polynomial exp2
+template <int D, int BOX, uint32_t POLY = 0x8888u>
 __global__ void __launch_bounds__(DN_THREADS, 1)
     dense_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
-                 const __grid_constant__ CUtensorMap tmq, AttnParams p) {
+                 const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmq1,
+                 AttnParams p) {
   constexpr int CH = D / 64;
   constexpr int EPB = DN_KB / BOX;      // page entries per 64-key block
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -175,7 +177,10 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
     // A unit whose tokens are consecutive rows of q (a prefill chunk) loads each 128-row
     // tile chunk with one 3-D TMA box {64 cols, g heads, 128/g tokens}; other units (a
     // SEPARATE node's tokens come from many requests) gather rows with cp.async.
-    if (lane == 0 && 128 % p.g == 0) ptx::tma_prefetch_desc(&tmq);
+    if (lane == 0 && 128 % p.g == 0) {
+      ptx::tma_prefetch_desc(&tmq);
+      ptx::tma_prefetch_desc(&tmq1);
+    }
     uint32_t gu = 0;
     for (int ui = blockIdx.x; ui < p.n_units; ui += gridDim.x, ++gu) {
       const Unit u = p.units[ui];
@@ -195,13 +200,40 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         __syncwarp();
         continue;
       }
-      for (int row = lane; row < nrows; row += 32) {
+      if (128 % p.g == 0) {
+        // tokens from many requests (a SEPARATE node): one TMA box {64, g, 1} per token and
+        // 64-column chunk, issued by the lanes in parallel (each box = g whole rows)
+        const int ntok = (u.n_rows + p.g - 1) / p.g, tpt = 128 / p.g;
+        if (lane == 0) ptx::mbar_arrive_expect_tx(q_full, (uint32_t)(ntok * CH * p.g * 128));
+        __syncwarp();
+        for (int i = lane; i < ntok; i += 32) {
+          const int tok = p.item_tokens[u.tok_base + u.row_begin / p.g + i];
+          uint8_t* dst = smem + (i >= tpt ? L.q1 : L.q0) + (i % tpt) * p.g * 128;
+#pragma unroll
+          for (int c = 0; c < CH; ++c) ptx::tma_load_3d(dst + c * DN_QCHUNK, &tmq1, q_full, c * 64, u.kvh * p.g, tok);
+        }
+        continue;
+      }
+      // all of this lane's row tokens are requested before any is used (one round trip,
+      // not one per row)
+      int32_t qrow[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int row = lane + 32 * k;
+        qrow[k] = -1;
+        if (row < nrows && row < u.n_rows) {
+          const int ir = u.row_begin + row, tl = ir / p.g;
+          qrow[k] = p.item_tokens[u.tok_base + tl] * p.hq + u.kvh * p.g + (ir - tl * p.g);
+        }
+      }
+#pragma unroll 1
+      for (int k = 0; k < 8; ++k) {   // (the loader warp runs under setmaxnreg 56)
+        const int row = lane + 32 * k;
+        if (row >= nrows) break;
         uint8_t* qs = smem + ((row >> 7) ? L.q1 : L.q0);
         const int r = row & 127;
-        if (row < u.n_rows) {
-          const RowInfo ri = row_info(p, u, row);
-          const __nv_bfloat16* src =
-              reinterpret_cast<const __nv_bfloat16*>(p.q) + ((int64_t)ri.token * p.hq + ri.head) * D;
+        if (qrow[k] >= 0) {
+          const __nv_bfloat16* src = reinterpret_cast<const __nv_bfloat16*>(p.q) + (int64_t)qrow[k] * D;
 #pragma unroll
           for (int c = 0; c < D / 8; ++c)
             ptx::cp_async16(qs + (c / 8) * DN_QCHUNK + ptx::sw128(r, c % 8), src + 8 * c);
@@ -336,11 +368,13 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       const int row = 128 * t + r;                    // row within the unit
       int32_t pos = INT32_MIN, token = 0, head = 0, tgt = PM_SKIP;
       if (row < u.n_rows) {
-        RowInfo ri = row_info(p, u, row);
-        pos = p.tok_pos[ri.token];
-        token = ri.token;
-        head = ri.head;
-        tgt = row_target(p, u, ri.tl);
+        // a TMA-loaded unit's tokens are consecutive from dqtok: no item_tokens round trip
+        const int qt0 = p.dqtok[ui];
+        const int ir = u.row_begin + row, tl = ir / p.g;
+        tgt = row_target(p, u, tl);
+        token = qt0 >= 0 ? qt0 + (tl - u.row_begin / p.g) : p.item_tokens[u.tok_base + tl];
+        head = u.kvh * p.g + (ir - tl * p.g);
+        pos = p.tok_pos[token];
       }
       float m_ref = -INFINITY, l = 0.f;
       int2 am = make_int2(-1, 0);                     // {merge list, sources} of a partial row
@@ -424,7 +458,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
             const int key = c * 32 + 2 * k;
             const uint64_t x2 = ptx::ffma2(ptx::f2pack(sv[key], sv[key + 1]), sc2, nm2);
             uint64_t p2;
-            if ((k & 3) == 3) {
+            if ((POLY >> k) & 1u) {
               p2 = ptx::exp2_poly2(x2);
             } else {
               float x0, x1;
@@ -456,6 +490,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         ptx::mbar_wait(&o_done[t * 2 + lb], ((lb ? scnt1 : scnt0) - 1) & 1);
       }
       ptx::tc_fence_after();
+      if (threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 60);
       const float m_use = m_ref == -INFINITY ? 0.f : m_ref;
       const float inv = l > 0.f ? 1.f / l : 0.f;
       const float lse2 = l > 0.f ? m_use + log2f(l) : -INFINITY;
@@ -478,33 +513,42 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
           rp[s_] = reinterpret_cast<char*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(rowp), rr));
           rk[s_] = __shfl_sync(0xffffffffu, kind, rr);
         }
+        // TMEM column loads two chunks at a time (one wait per 64 columns; 128 columns
+        // at once would exceed the 168-register compile-time budget), then chunk by chunk
+        // through the staging tile
 #pragma unroll 1
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t ov[32];
-          ptx::tmem_ld32(tmem + lane_base + col_o + c * 32, ov);
-          ptx::tmem_wait_ld();
+        for (int hh = 0; hh < D / 64; ++hh) {
+         uint32_t ov2[64];
+         ptx::tmem_ld32(tmem + lane_base + col_o + hh * 64, ov2);
+         ptx::tmem_ld32(tmem + lane_base + col_o + hh * 64 + 32, ov2 + 32);
+         ptx::tmem_wait_ld();
+         if (hh == 0 && threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 62);
+#pragma unroll
+         for (int cc = 0; cc < 2; ++cc) {
+          const int c = 2 * hh + cc;
+          const uint32_t* ov = ov2 + 32 * cc;
 #pragma unroll
           for (int u8 = 0; u8 < 8; ++u8)
             ptx::sts128(stg + ptx::sw128(lane, u8), __uint_as_float(ov[4 * u8]) * inv,
                         __uint_as_float(ov[4 * u8 + 1]) * inv, __uint_as_float(ov[4 * u8 + 2]) * inv,
                         __uint_as_float(ov[4 * u8 + 3]) * inv);
           __syncwarp();
+          float4 v[8];   // all eight row segments in flight before the first store
+#pragma unroll
+          for (int s_ = 0; s_ < 8; ++s_) v[s_] = ptx::lds128(stg + ptx::sw128(s_ * 4 + (lane >> 3), k8));
 #pragma unroll
           for (int s_ = 0; s_ < 8; ++s_) {
-            const int rr = s_ * 4 + (lane >> 3);
-            const float4 v = ptx::lds128(stg + ptx::sw128(rr, k8));
-            if (rk[s_] == 2) {
-              *reinterpret_cast<float4*>(rp[s_] + c * 128 + k8 * 16) = v;
-            } else if (rk[s_] == 1) {
-              uint2 b;
-              b.x = ptx::pack_bf16(v.x, v.y);
-              b.y = ptx::pack_bf16(v.z, v.w);
-              *reinterpret_cast<uint2*>(rp[s_] + c * 64 + k8 * 8) = b;
-            }
+            if (rk[s_] == 2)
+              ptx::stg128(rp[s_] + c * 128 + k8 * 16, v[s_]);
+            else if (rk[s_] == 1)
+              ptx::stg64(rp[s_] + c * 64 + k8 * 8, ptx::pack_bf16(v[s_].x, v[s_].y), ptx::pack_bf16(v[s_].z, v[s_].w));
           }
           __syncwarp();   // the staging tile is rewritten by the next chunk
+          if (c == 0 && threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 63);
+         }
         }
       }
+      if (threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 61);
       if (tgt == PM_DIRECT) p.lse[(int64_t)token * p.hq + head] = lse2 * kLn2;
       else if (tgt >= 0) p.ws_lse[(int64_t)tgt * p.hq + head] = lse2;
       if (p.arrive != nullptr && tgt >= 0) {   // counts in at the next unit's epilogue (or the end)
@@ -529,7 +573,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
 }
 
 cudaError_t make_cache_tmap(CUtensorMap* m, const void* base, int64_t rows, int D, int box_rows);
-cudaError_t make_q_tmap(CUtensorMap* m, const void* base, int64_t T, int hq, int D, int g);
+cudaError_t make_q_tmap(CUtensorMap* m, const void* base, int64_t T, int hq, int D, int g, int box_tok);
 cudaError_t set_smem_once(const void* func, size_t bytes);
 int num_sms_cached();
 
@@ -541,17 +585,19 @@ static cudaError_t launch_dense_db(const AttnParams& p, int64_t n_cache_pages, c
   if (e != cudaSuccess) return e;
   e = make_cache_tmap(&tv, p.v_cache, rows, D, BOX);
   if (e != cudaSuccess) return e;
-  CUtensorMap tq;   // only dereferenced for units the planner marked (128 % g == 0)
+  CUtensorMap tq, tq1;   // Q boxes of 128/g tokens / of one token; only used when 128 % g == 0
   memset(&tq, 0, sizeof(tq));
+  memset(&tq1, 0, sizeof(tq1));
   if (128 % p.g == 0) {
-    e = make_q_tmap(&tq, p.q, p.n_tokens, p.hq, D, p.g);
+    e = make_q_tmap(&tq, p.q, p.n_tokens, p.hq, D, p.g, 128 / p.g);
+    if (e == cudaSuccess) e = make_q_tmap(&tq1, p.q, p.n_tokens, p.hq, D, p.g, 1);
     if (e != cudaSuccess) return e;
   }
   const size_t smem = dense_layout(D).total + 1024;
   e = set_smem_once((const void*)dense_kernel<D, BOX>, smem);
   if (e != cudaSuccess) return e;
   const int grid = p.n_units < num_sms_cached() ? p.n_units : num_sms_cached();
-  dense_kernel<D, BOX><<<grid, DN_THREADS, smem, st>>>(tk, tv, tq, p);
+  dense_kernel<D, BOX><<<grid, DN_THREADS, smem, st>>>(tk, tv, tq, tq1, p);
   return cudaPeekAtLastError();
 }
 

@@ -420,18 +420,18 @@ namespace {
 struct QmapEntry {
   const void* base;
   int64_t T;
-  int hq, D, g;
+  int hq, D, g, bt;
   CUtensorMap map;
 };
 QmapEntry g_qmaps[8];
 int g_qmap_n = 0, g_qmap_next = 0;
 }  // namespace
 
-cudaError_t make_q_tmap(CUtensorMap* m, const void* base, int64_t T, int hq, int D, int g) {
+cudaError_t make_q_tmap(CUtensorMap* m, const void* base, int64_t T, int hq, int D, int g, int box_tok) {
   std::lock_guard<std::mutex> lk(g_cache_mu);
   for (int i = 0; i < g_qmap_n; ++i) {
     const QmapEntry& t = g_qmaps[i];
-    if (t.base == base && t.T == T && t.hq == hq && t.D == D && t.g == g) {
+    if (t.base == base && t.T == T && t.hq == hq && t.D == D && t.g == g && t.bt == box_tok) {
       *m = t.map;
       return cudaSuccess;
     }
@@ -440,14 +440,14 @@ cudaError_t make_q_tmap(CUtensorMap* m, const void* base, int64_t T, int hq, int
   if (!enc) return cudaErrorNotSupported;
   cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)hq, (cuuint64_t)(T > 0 ? T : 1)};
   cuuint64_t strides[2] = {(cuuint64_t)D * 2, (cuuint64_t)hq * D * 2};
-  cuuint32_t box[3] = {64, (cuuint32_t)g, (cuuint32_t)(128 / g)};
+  cuuint32_t box[3] = {64, (cuuint32_t)g, (cuuint32_t)box_tok};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
   QmapEntry& t = g_qmaps[g_qmap_next];
-  t = {base, T, hq, D, g, *m};
+  t = {base, T, hq, D, g, box_tok, *m};
   g_qmap_next = (g_qmap_next + 1) % 8;
   if (g_qmap_n < 8) ++g_qmap_n;
   return cudaSuccess;

@@ -190,19 +190,25 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
     RowDesc d0, d1;        // rows g8 and g8 + 8 (softmax / output rows of this lane)
     int eb, ne;            // entry range
     int4 ebatch;           // entry eb + lane (lane < ne)
+    int32_t qrow;          // q row of this lane's Q-copy row (lane / 2), -1: padding
   };
-  // issue every load of unit idx; Q goes to buffer buf by cp.async
-  auto prefetch = [&](const int4 ann, int buf) -> Pre {
+  // issue every metadata load of the announced unit (none is used here, so no stall)
+  auto prefetch = [&](const int4 ann) -> Pre {
     Pre r;
     const RowDesc* rd = p.srows + (int64_t)ann.x * STREAM_ROWS;
-    const RowDesc dq = rd[lane >> 1];
+    r.qrow = rd[lane >> 1].qrow;
     r.d0 = rd[g8];
     r.d1 = rd[g8 + 8];
     r.eb = ann.y;
     r.ne = ann.z;
     r.ebatch = lane < r.ne ? ents[r.eb + lane] : make_int4(0, 0, 0, 0);
-    const bool valid = dq.qrow >= 0;
-    const __nv_bfloat16* src = reinterpret_cast<const __nv_bfloat16*>(p.q) + (valid ? (int64_t)dq.qrow * D : 0);
+    return r;
+  };
+  // the next unit's Q rows (cp.async into buffer buf), issued once the current unit's
+  // first stage is done: by then its row descriptors have arrived
+  auto issue_q = [&](const Pre& r, int buf) {
+    const bool valid = r.qrow >= 0;
+    const __nv_bfloat16* src = reinterpret_cast<const __nv_bfloat16*>(p.q) + (valid ? (int64_t)r.qrow * D : 0);
 #pragma unroll
     for (int k = 0; k < CPL; ++k) {
       const int unit16 = (lane & 1) * CPL + k;
@@ -210,7 +216,6 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
                             src + 8 * unit16, valid);
     }
     ptx::cp_async_commit();
-    return r;
   };
 
   // Arrival merging, deferred by one unit: the rows of the unit before count in (and
@@ -235,7 +240,10 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
   };
   int4 nann = next_index();
   Pre pre{};
-  if (nann.x < p.n_units) pre = prefetch(nann, 0);
+  if (nann.x < p.n_units) {
+    pre = prefetch(nann);
+    issue_q(pre, 0);
+  }
   for (int buf = 0; nann.x < p.n_units; buf ^= 1) {
     const Pre cu = pre;
     ptx::cp_async_wait_group0();
@@ -251,7 +259,8 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
     }
     __syncwarp();   // every lane's ldmatrix of this buffer is done before the next prefetch targets it later
     nann = next_index();
-    if (nann.x < p.n_units) pre = prefetch(nann, buf ^ 1);
+    bool q_pending = nann.x < p.n_units;
+    if (q_pending) pre = prefetch(nann);
     const int32_t pos0r = cu.d0.qrow >= 0 ? cu.d0.pos : INT32_MIN;
     const int32_t pos1r = cu.d1.qrow >= 0 ? cu.d1.pos : INT32_MIN;
 
@@ -358,8 +367,13 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
         }
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&wempty[s]);
+        if (q_pending) {
+          issue_q(pre, buf ^ 1);
+          q_pending = false;
+        }
       }
     }
+    if (q_pending) issue_q(pre, buf ^ 1);
     // ---- unit end: the previous unit's partial rows count in (their stores are long
     // complete, so the release fence is cheap), then this unit's rows are written
     if (p.arrive != nullptr) settle();

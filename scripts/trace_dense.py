@@ -30,9 +30,9 @@ used = t[:, 0] > 0
 t = t[used]
 t0 = t[:, 0].min()
 rel = np.where(t > 0, (t - t0) / 1e3, np.nan)   # us
-names = {0: "start", 1: "setup", 2: "mma_q", 3: "tma0", 4: "epi0", 5: "epi1", 6: "exit"}
+names = {0: "start", 1: "setup", 2: "mma_q", 3: "tma0", 4: "epi0", 5: "epi1", 6: "exit", 60: "o_done", 61: "stored", 62: "ld_c0", 63: "st_c0"}
 print(f"{w.name}: {used.sum()} CTAs, dense units {db.info['n_dense_units']}")
-for k in list(range(7)) + list(range(8, 40)):
+for k in list(range(7)) + [60, 62, 63, 61] + list(range(8, 40)):
     col = rel[:, k]
     if np.all(np.isnan(col)):
         continue
