@@ -29,6 +29,8 @@ extern "C" int blend_internal_set_trace(void* dev) {
   return 0;
 }
 
+static bool blockIdx_trace_ok(int) { return true; }
+
 namespace {
 int cuda_fail(cudaError_t e) { return blend_internal_fail(BLEND_ECUDA, cudaGetErrorString(e)); }
 
@@ -162,6 +164,7 @@ extern "C" int blend_attention(const blend_attn_args* a, void* stream) {
   ps_.n_units = (int32_t)pl.count[SEC_STREAM_UNITS];
   ps_.avg_entries = ps_.n_units > 0 ? (int32_t)(pl.count[SEC_COUNT + 1] / ps_.n_units) : 0;
   ps_.arrive = arrive;
+  ps_.trace = blockIdx_trace_ok(ps_.n_units) ? g_trace : nullptr;
   if (generic) e = launch_generic(ps_, st);
   else if (n_merge_all != n_merge_unfused) e = launch_stream(ps_, a->n_cache_pages, st, overlap);   // fused merges
   else e = launch_streamw(ps_, a->n_cache_pages, st, overlap);

@@ -51,6 +51,14 @@ __device__ __forceinline__ void trace_stamp(const AttnParams& p, int k) {
     p.trace[(size_t)blockIdx.x * 64 + k] = t;
   }
 }
+// streaming-pass diagnostics: the second half of the trace buffer ([148 + CTA][64])
+__device__ __forceinline__ void trace_stamp_s(const AttnParams& p, int k) {
+  if (p.trace != nullptr && k < 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[(size_t)(148 + blockIdx.x) * 64 + k] = t;
+  }
+}
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z += 0x9E3779B97F4A7C15ull;

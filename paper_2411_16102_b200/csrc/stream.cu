@@ -113,6 +113,10 @@ __global__ void __launch_bounds__(ST_THREADS, 2)
         }
       }
     }
+    // Lanes 1..31 must not reach griddepcontrol.wait while lane 0 still issues loads:
+    // the wait parks the whole warp until the dense grid completes (measured: the
+    // producer stalled ~13 us on C2 and the overlap was lost).
+    __syncwarp();
     ptx::pdl_wait();   // this grid completes only after the (overlapped) dense grid has completed
     return;
   }

@@ -28,6 +28,7 @@ namespace blend {
 constexpr int SW_WARPS = 4;                  // consumer warps = rings = producer warps
 constexpr int SW_THREADS = 32 * (2 * SW_WARPS);
 constexpr int SW_STAGES = 3;
+constexpr int SW_STATIC = 0;                 // statically assigned units per ring (0: all dynamic, measured best)
 constexpr int SW_KEYS = 32;                  // keys per stage (half a 64-slot entry)
 constexpr int SW_CHUNK = SW_KEYS * 128;      // 32 rows x 128 B
 
@@ -65,6 +66,7 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
   uint64_t* uqe = uqf + SW_WARPS * 2;             // [ring][2] announcement consumed
   int4* uq = reinterpret_cast<int4*>(smem + L.uq);   // [ring][2] {unit (>= n_units: done), entry begin, count}
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) trace_stamp_s(p, 0);
   ptx::pdl_launch_dependents();
 
   if (threadIdx.x == 0) {
@@ -106,8 +108,25 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
       // Unit pipeline, two deep: while unit k's stages are issued, unit k+1 is known
       // (struct loaded, announced, first entry requested) and unit k+2's index is being
       // fetched from the counter, so no dependent global load sits between two units.
-      int i_cur = atomicAdd(p.sched, 1);
-      int i_nxt = atomicAdd(p.sched, 1);
+      // The first SW_STATIC units of every ring are assigned statically (round-robin over
+      // the longest-first order); the rest are handed out by the counter.  Measured on
+      // B200: while the overlapped dense grid runs, a same-address atomicAdd by the
+      // streaming producers can take ~10 us to return, so the counter stays off the
+      // start-up path.
+      const int R = (int)gridDim.x * SW_WARPS, ring_id = (int)blockIdx.x * SW_WARPS + w;
+      const int nstat = n / R < SW_STATIC ? n / R : SW_STATIC;
+      int k_next = 0;   // units of this ring handed out so far
+      auto fetch = [&]() -> int {
+        const int k = k_next++;
+        if (k < nstat) return k * R + ring_id;
+        // plain atom (no warp aggregation: that would shuffle the result right away and
+        // wait for it); the result is first used one unit later
+        int v;
+        asm volatile("atom.global.add.s32 %0, [%1], 1;" : "=r"(v) : "l"(p.sched) : "memory");
+        return nstat * R + v;
+      };
+      int i_cur = fetch();
+      int i_nxt = fetch();
       Unit u_cur = i_cur < n ? p.units[i_cur] : Unit{};
       announce(i_cur, u_cur);
       int4 cur = i_cur < n ? ents[u_cur.entry_begin] : make_int4(0, 0, 0, 0);
@@ -122,7 +141,7 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
             announce(i_nxt, u_nxt);
             if (i_nxt < n) {
               nfirst = ents[u_nxt.entry_begin];
-              i_nn = atomicAdd(p.sched, 1);
+              i_nn = fetch();
             }
             phase = 2;
           }
@@ -159,6 +178,10 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
         i_nxt = i_nn;
       }
     }
+    // Lanes 1..31 must not reach griddepcontrol.wait while lane 0 still issues loads:
+    // the wait parks the whole warp until the dense grid completes (measured: the
+    // producer stalled ~13 us on C2 and the overlap was lost).
+    __syncwarp();
     ptx::pdl_wait();   // this grid completes only after the (overlapped) dense grid has completed
     return;
   }
@@ -244,7 +267,9 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
     pre = prefetch(nann);
     issue_q(pre, 0);
   }
-  for (int buf = 0; nann.x < p.n_units; buf ^= 1) {
+  int tu = 0;   // diagnostics: units done by this warp
+  for (int buf = 0; nann.x < p.n_units; buf ^= 1, ++tu) {
+    if (warp == 0 && lane == 0) trace_stamp_s(p, 2 + 4 * tu);
     const Pre cu = pre;
     ptx::cp_async_wait_group0();
     __syncwarp();
@@ -284,6 +309,7 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
         const int kbase = h * SW_KEYS;                 // slot of key 0 of this stage
         const int nvalid = en_count - kbase;           // >= 1
         ptx::mbar_wait(&wfull[s], ph);
+        if (warp == 0 && lane == 0 && k == 0 && h == 0) trace_stamp_s(p, 3 + 4 * tu);
         const uint32_t kst = ptx::smem_u32(ring + s * L.stage_stride);
         const uint32_t vst = kst + CH * SW_CHUNK;
         const int ntv = nvalid >= SW_KEYS ? 4 : (nvalid + 7) / 8;   // n-tiles holding valid keys
@@ -374,6 +400,7 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
       }
     }
     if (q_pending) issue_q(pre, buf ^ 1);
+    if (warp == 0 && lane == 0) trace_stamp_s(p, 4 + 4 * tu);
     // ---- unit end: the previous unit's partial rows count in (their stores are long
     // complete, so the release fence is cheap), then this unit's rows are written
     if (p.arrive != nullptr) settle();
@@ -409,6 +436,7 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
       pend0 = cu.d0;
       pend1 = cu.d1;
     }
+    if (warp == 0 && lane == 0) trace_stamp_s(p, 5 + 4 * tu);
   }
   if (p.arrive != nullptr) settle();
   ptx::pdl_wait();

@@ -18,14 +18,14 @@ db = device_batch(w, tree_kw=dict(num_sms=148))
 for _ in range(3):
     db.run()
 torch.cuda.synchronize()
-tr = torch.zeros((148, 64), dtype=torch.int64, device="cuda")
+tr = torch.zeros((296, 64), dtype=torch.int64, device="cuda")   # dense rows 0..147, streaming 148..295
 L = B.lib()
 L.blend_internal_set_trace.argtypes = [C.c_void_p]
 L.blend_internal_set_trace(tr.data_ptr())
 db.run(flags=B.SERIALIZE)
 torch.cuda.synchronize()
 L.blend_internal_set_trace(None)
-t = tr.cpu().numpy().astype(np.float64)
+t = tr.cpu().numpy().astype(np.float64)[:148]
 used = t[:, 0] > 0
 t = t[used]
 t0 = t[:, 0].min()
