@@ -173,6 +173,7 @@ extern "C" int blend_attention(const blend_attn_args* a, void* stream) {
   if (a->events[2]) cudaEventRecord((cudaEvent_t)a->events[2], st);
   AttnParams pm = p;
   pm.n_merge = (int32_t)pl.count[SEC_COUNT + 2];   // fused lists are merged by the streaming pass
+  pm.trace = g_trace;
   if (!arrival) {
     e = launch_merge(pm, st, overlap);
     if (e != cudaSuccess) return cuda_fail(e);

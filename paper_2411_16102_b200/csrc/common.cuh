@@ -224,44 +224,59 @@ __device__ __forceinline__ bool arrive_last(const AttnParams& p, int32_t first, 
 template <int D>
 __device__ __forceinline__ void merge_row4(const AttnParams& p, int first, int nsrc, int h, int qrow, int sub) {
   constexpr int E = D / 4;
-  float mx = -INFINITY;
-  for (int i = 0; i < nsrc; ++i) mx = fmaxf(mx, __ldcg(p.ws_lse + (int64_t)(first + i) * p.hq + h));
+  // one online pass over the sources, two at a time: both sources' lse and o loads are
+  // in flight together (one memory round trip per pair), then a rescale-accumulate
+  float mx = -INFINITY, tot = 0.f;
   float acc[E];
 #pragma unroll
   for (int k = 0; k < E; ++k) acc[k] = 0.f;
-  float tot = 0.f;
-  if (mx != -INFINITY) {
-#pragma unroll 2
-    for (int i = 0; i < nsrc; ++i) {
-      const int64_t row = (int64_t)(first + i) * p.hq + h;
-      const float w = exp2f(__ldcg(p.ws_lse + row) - mx);   // empty partial: lse = -inf -> 0
-      tot += w;
-      const float4* src = reinterpret_cast<const float4*>(p.ws_o + row * D + sub * E);
+  for (int i = 0; i < nsrc; i += 2) {
+    const bool two = i + 1 < nsrc;
+    const int64_t r0 = (int64_t)(first + i) * p.hq + h, r1 = two ? r0 + p.hq : r0;
+    const float l0 = __ldcg(p.ws_lse + r0), l1 = two ? __ldcg(p.ws_lse + r1) : -INFINITY;
+    float4 v0[E / 4], v1[E / 4];
+    const float4* s0 = reinterpret_cast<const float4*>(p.ws_o + r0 * D + sub * E);
+    const float4* s1 = reinterpret_cast<const float4*>(p.ws_o + r1 * D + sub * E);
 #pragma unroll
-      for (int k = 0; k < E / 4; ++k) {
-        const float4 v = __ldcg(src + k);
-        acc[4 * k] = fmaf(w, v.x, acc[4 * k]);
-        acc[4 * k + 1] = fmaf(w, v.y, acc[4 * k + 1]);
-        acc[4 * k + 2] = fmaf(w, v.z, acc[4 * k + 2]);
-        acc[4 * k + 3] = fmaf(w, v.w, acc[4 * k + 3]);
-      }
+    for (int k = 0; k < E / 4; ++k) {
+      v0[k] = __ldcg(s0 + k);
+      v1[k] = __ldcg(s1 + k);
     }
+    const float cm = fmaxf(mx, fmaxf(l0, l1));
+    if (cm == -INFINITY) continue;                  // both empty so far
+    const float a = exp2f(mx - cm), w0 = exp2f(l0 - cm), w1 = exp2f(l1 - cm);   // -inf -> 0
+    tot = tot * a + w0 + w1;
+#pragma unroll
+    for (int k = 0; k < E / 4; ++k) {
+      acc[4 * k] = fmaf(w1, v1[k].x, fmaf(w0, v0[k].x, acc[4 * k] * a));
+      acc[4 * k + 1] = fmaf(w1, v1[k].y, fmaf(w0, v0[k].y, acc[4 * k + 1] * a));
+      acc[4 * k + 2] = fmaf(w1, v1[k].z, fmaf(w0, v0[k].z, acc[4 * k + 2] * a));
+      acc[4 * k + 3] = fmaf(w1, v1[k].w, fmaf(w0, v0[k].w, acc[4 * k + 3] * a));
+    }
+    mx = cm;
   }
   const float inv = tot > 0.f ? 1.f / tot : 0.f;
-  uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.out) + (int64_t)qrow * D + sub * E);
+  if (p.kv_f32) {
+    float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + (int64_t)qrow * D + sub * E);
 #pragma unroll
-  for (int k = 0; k < E / 8; ++k) {
-    uint4 w4;
-    __nv_bfloat162 b;
-    b = __floats2bfloat162_rn(acc[8 * k] * inv, acc[8 * k + 1] * inv);
-    w4.x = *reinterpret_cast<uint32_t*>(&b);
-    b = __floats2bfloat162_rn(acc[8 * k + 2] * inv, acc[8 * k + 3] * inv);
-    w4.y = *reinterpret_cast<uint32_t*>(&b);
-    b = __floats2bfloat162_rn(acc[8 * k + 4] * inv, acc[8 * k + 5] * inv);
-    w4.z = *reinterpret_cast<uint32_t*>(&b);
-    b = __floats2bfloat162_rn(acc[8 * k + 6] * inv, acc[8 * k + 7] * inv);
-    w4.w = *reinterpret_cast<uint32_t*>(&b);
-    dst[k] = w4;
+    for (int k = 0; k < E / 4; ++k)
+      dst[k] = make_float4(acc[4 * k] * inv, acc[4 * k + 1] * inv, acc[4 * k + 2] * inv, acc[4 * k + 3] * inv);
+  } else {
+    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.out) + (int64_t)qrow * D + sub * E);
+#pragma unroll
+    for (int k = 0; k < E / 8; ++k) {
+      uint4 w4;
+      __nv_bfloat162 b;
+      b = __floats2bfloat162_rn(acc[8 * k] * inv, acc[8 * k + 1] * inv);
+      w4.x = *reinterpret_cast<uint32_t*>(&b);
+      b = __floats2bfloat162_rn(acc[8 * k + 2] * inv, acc[8 * k + 3] * inv);
+      w4.y = *reinterpret_cast<uint32_t*>(&b);
+      b = __floats2bfloat162_rn(acc[8 * k + 4] * inv, acc[8 * k + 5] * inv);
+      w4.z = *reinterpret_cast<uint32_t*>(&b);
+      b = __floats2bfloat162_rn(acc[8 * k + 6] * inv, acc[8 * k + 7] * inv);
+      w4.w = *reinterpret_cast<uint32_t*>(&b);
+      dst[k] = w4;
+    }
   }
   if (sub == 0) p.lse[qrow] = mx != -INFINITY ? (mx + log2f(tot)) * kLn2 : -INFINITY;
 }

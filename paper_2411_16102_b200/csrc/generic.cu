@@ -149,9 +149,18 @@ __global__ void __launch_bounds__(128) generic_unit_kernel(AttnParams p) {
 // One warp per (merged token, q head); lanes own D/32 contiguous elements.
 __global__ void __launch_bounds__(256) merge_kernel(AttnParams p) {
   ptx::pdl_wait();   // launched as a programmatic dependent of the streaming pass
+  if (p.trace != nullptr && threadIdx.x == 0) {   // diagnostics: first start / last end
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMin(p.trace + 296 * 64, t);
+  }
   const int h = blockIdx.y * 8 + (threadIdx.x >> 5);
-  if (h >= p.hq) return;
-  warp_merge_row(p, blockIdx.x, h, threadIdx.x & 31);
+  if (h < p.hq) warp_merge_row(p, blockIdx.x, h, threadIdx.x & 31);
+  if (p.trace != nullptr && (threadIdx.x & 31) == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMax(p.trace + 296 * 64 + 1, t);
+  }
 }
 
 cudaError_t set_smem_once(const void* func, size_t bytes);

@@ -19,7 +19,8 @@ db = device_batch(w, tree_kw=dict(num_sms=148))
 for _ in range(3):
     db.run()
 torch.cuda.synchronize()
-tr = torch.zeros((296, 64), dtype=torch.int64, device="cuda")
+tr = torch.zeros((297, 64), dtype=torch.int64, device="cuda")
+tr[296, 0] = 2**62   # merge kernel: first start (atomicMin), last end (atomicMax)
 L = B.lib()
 L.blend_internal_set_trace.argtypes = [C.c_void_p]
 L.blend_internal_set_trace(tr.data_ptr())
@@ -28,7 +29,7 @@ torch.cuda.synchronize()
 L.blend_internal_set_trace(None)
 t = tr.cpu().numpy().astype(np.float64)
 t0 = t[:148, 0][t[:148, 0] > 0].min() if (t[:148, 0] > 0).any() else t[148:, 0][t[148:, 0] > 0].min()
-s = t[148:]
+s = t[148:296]
 s = s[s[:, 0] > 0]
 rel = np.where(s > 0, (s - t0) / 1e3, np.nan)
 print(f"{w.name}: {len(s)} streaming CTAs (flags={flags}); dense CTAs {(t[:148, 0] > 0).sum()}")
@@ -41,4 +42,10 @@ for u in range(14):
     n = int(np.sum(~np.isnan(rel[:, cols[0]])))
     print(f"  unit {u}: start {st:7.2f} data {fd:7.2f} kv_end {ke:7.2f} end {en:7.2f}  ({n} CTAs)")
 last = np.nanmax(rel[:, 2:38], axis=1)
+d6 = t[:148, 6][t[:148, 6] > 0]
+if len(d6):
+    print(f"  dense CTA exit: median {np.median((d6 - t0) / 1e3):.2f} max {np.max((d6 - t0) / 1e3):.2f} us")
+m0, m1 = t[296, 0], t[296, 1]
+if 0 < m0 < 2**62:
+    print(f"  merge kernel: first start {(m0 - t0) / 1e3:.2f} us, last end {(m1 - t0) / 1e3:.2f} us")
 print(f"  warp-0 last stamp: median {np.nanmedian(last):.2f} max {np.nanmax(last):.2f}")
