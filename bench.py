@@ -186,12 +186,18 @@ def cpu_baseline(w, budget_s=15.0):
     # calibrate: ~1 GFLOP/s per core for fp64 einsum is conservative
     reqs, f = oracle_sample(w, budget_flops=budget_s * cores * 1.0e9)
     t_math, wall = time_oracle(w, reqs, cores)
+    reps = 1
+    while t_math * reps < 0.3 * budget_s and reps < 64:   # small workloads: repeat for a stable time
+        t2, _ = time_oracle(w, reqs, cores)
+        t_math = (t_math * reps + t2) / (reps + 1)
+        reps += 1
     f_s = float(f[reqs].sum())
     f_all = float(f.sum())
     t_full = t_math * f_all / f_s
     return {"value": w.sum_q / t_full, "unit": "tokens/s", "cores": cores, "kind": "oracle",
             "sample": f"{len(reqs)} of {w.n_req} requests (stratified), fp64 numpy, "
-                      f"{t_math:.2f} s math on {cores} cores; extrapolated by F_alg share {f_s / f_all:.4f}",
+                      f"{t_math:.3f} s math per pass on {cores} cores (mean of {reps} passes); "
+                      f"extrapolated by F_alg share {f_s / f_all:.4f}",
             "measured_s": t_math, "extrapolated_step_s": t_full}
 
 
