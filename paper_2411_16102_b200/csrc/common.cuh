@@ -141,7 +141,10 @@ __device__ __forceinline__ void fused_merge_store(const AttnParams& p, int32_t t
 // dependent loads are merge_off -> partials;
 // lanes own D/32 contiguous elements.  Partials are read through L2 (ld.global.cg):
 // with arrival merging they were written by other SMs during this launch.
-__device__ __forceinline__ void warp_merge_row(const AttnParams& p, int m, int h, int lane) {
+template <int NH>
+__device__ __forceinline__ void warp_merge_heads(const AttnParams& p, int m, int h0, int lane) {
+  // NH q heads of merge list m per warp: both heads' loads of a chunk are in flight
+  // together (half the warps of one head per warp, so the grid fits one wave)
   const int token = p.merge_tok[m];
   const int s0 = p.merge_off[m], s1 = p.merge_off[m + 1];
   const int D = p.d;
@@ -149,54 +152,69 @@ __device__ __forceinline__ void warp_merge_row(const AttnParams& p, int m, int h
   const int e0 = lane * vec;
   // One pass in chunks of MCH sources: every load of a chunk is issued before any is
   // used (rows -> lse -> o are the only dependent steps), then an online rescale.
-  constexpr int MCH = 4;
-  float mx = -INFINITY, tot = 0.f;
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  constexpr int MCH = 2;
+  float mx[NH], tot[NH], acc[NH][4];
+#pragma unroll
+  for (int j = 0; j < NH; ++j) {
+    mx[j] = -INFINITY;
+    tot[j] = 0.f;
+    acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+  }
   for (int c0 = s0; c0 < s1; c0 += MCH) {
-    int64_t row[MCH];
-    float l[MCH];
-    float4 v[MCH];
+    float l[NH][MCH];
+    float4 v[NH][MCH];
 #pragma unroll
-    for (int i = 0; i < MCH; ++i) row[i] = c0 + i < s1 ? (int64_t)(c0 + i) : -1;   // unfused: row s = entry s
+    for (int j = 0; j < NH; ++j) {
+      const int h = h0 + j < p.hq ? h0 + j : h0;
 #pragma unroll
-    for (int i = 0; i < MCH; ++i) l[i] = row[i] >= 0 ? __ldcg(p.ws_lse + row[i] * p.hq + h) : -INFINITY;
-#pragma unroll
-    for (int i = 0; i < MCH; ++i) {
-      v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (row[i] >= 0) {
-        const float* src = p.ws_o + (row[i] * p.hq + h) * D + e0;
-        if (vec == 4) {
-          v[i] = __ldcg(reinterpret_cast<const float4*>(src));
-        } else {
-          const float2 t = __ldcg(reinterpret_cast<const float2*>(src));
-          v[i].x = t.x;
-          v[i].y = t.y;
+      for (int i = 0; i < MCH; ++i) {
+        const int64_t row = c0 + i;   // unfused: entry s is partial row s
+        const bool ok = c0 + i < s1;
+        l[j][i] = ok ? __ldcg(p.ws_lse + row * p.hq + h) : -INFINITY;
+        v[j][i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (ok) {
+          const float* src = p.ws_o + (row * p.hq + h) * D + e0;
+          if (vec == 4) {
+            v[j][i] = __ldcg(reinterpret_cast<const float4*>(src));
+          } else {
+            const float2 t = __ldcg(reinterpret_cast<const float2*>(src));
+            v[j][i].x = t.x;
+            v[j][i].y = t.y;
+          }
         }
       }
     }
-    float cm = mx;
 #pragma unroll
-    for (int i = 0; i < MCH; ++i) cm = fmaxf(cm, l[i]);
-    if (cm == -INFINITY) continue;
-    const float a = exp2f(mx - cm);      // mx = -inf on the first live chunk -> 0
-    tot *= a;
+    for (int j = 0; j < NH; ++j) {
+      float cm = mx[j];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) acc[k] *= a;
+      for (int i = 0; i < MCH; ++i) cm = fmaxf(cm, l[j][i]);
+      if (cm == -INFINITY) continue;
+      const float a = exp2f(mx[j] - cm);      // mx = -inf on the first live chunk -> 0
+      tot[j] *= a;
 #pragma unroll
-    for (int i = 0; i < MCH; ++i) {
-      const float w = exp2f(l[i] - cm);  // l = -inf (absent source) -> 0
-      tot += w;
-      acc[0] = fmaf(w, v[i].x, acc[0]);
-      acc[1] = fmaf(w, v[i].y, acc[1]);
-      acc[2] = fmaf(w, v[i].z, acc[2]);
-      acc[3] = fmaf(w, v[i].w, acc[3]);
+      for (int k = 0; k < 4; ++k) acc[j][k] *= a;
+#pragma unroll
+      for (int i = 0; i < MCH; ++i) {
+        const float w = exp2f(l[j][i] - cm);  // l = -inf (absent source) -> 0
+        tot[j] += w;
+        acc[j][0] = fmaf(w, v[j][i].x, acc[j][0]);
+        acc[j][1] = fmaf(w, v[j][i].y, acc[j][1]);
+        acc[j][2] = fmaf(w, v[j][i].z, acc[j][2]);
+        acc[j][3] = fmaf(w, v[j][i].w, acc[j][3]);
+      }
+      mx[j] = cm;
     }
-    mx = cm;
   }
-  const float inv = tot > 0.f ? 1.f / tot : 0.f;
-  const int64_t ob = ((int64_t)token * p.hq + h) * D + e0;
-  for (int k = 0; k < vec; ++k) st_elem(p.out, ob + k, acc[k] * inv, p.kv_f32);
-  if (lane == 0) p.lse[(int64_t)token * p.hq + h] = mx != -INFINITY ? (mx + log2f(tot)) * kLn2 : -INFINITY;
+#pragma unroll
+  for (int j = 0; j < NH; ++j) {
+    const int h = h0 + j;
+    if (h >= p.hq) break;
+    const float inv = tot[j] > 0.f ? 1.f / tot[j] : 0.f;
+    const int64_t ob = ((int64_t)token * p.hq + h) * D + e0;
+    for (int k = 0; k < vec; ++k) st_elem(p.out, ob + k, acc[j][k] * inv, p.kv_f32);
+    if (lane == 0) p.lse[(int64_t)token * p.hq + h] = mx[j] != -INFINITY ? (mx[j] + log2f(tot[j])) * kLn2 : -INFINITY;
+  }
 }
 
 // Arrival merging ("the last producer merges", replaces the merge launch).  A producer

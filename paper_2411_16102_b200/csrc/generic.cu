@@ -146,16 +146,16 @@ __global__ void __launch_bounds__(128) generic_unit_kernel(AttnParams p) {
   }
 }
 
-// One warp per (merged token, q head); lanes own D/32 contiguous elements.
-__global__ void __launch_bounds__(256) merge_kernel(AttnParams p) {
+// One warp per (merged token, 2 q heads); lanes own D/32 contiguous elements.
+__global__ void __launch_bounds__(256, 4) merge_kernel(AttnParams p) {   // 4 blocks/SM: one wave at C2
   ptx::pdl_wait();   // launched as a programmatic dependent of the streaming pass
   if (p.trace != nullptr && threadIdx.x == 0) {   // diagnostics: first start / last end
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     atomicMin(p.trace + 296 * 64, t);
   }
-  const int h = blockIdx.y * 8 + (threadIdx.x >> 5);
-  if (h < p.hq) warp_merge_row(p, blockIdx.x, h, threadIdx.x & 31);
+  const int h0 = (blockIdx.y * 8 + (threadIdx.x >> 5)) * 2;   // two q heads per warp
+  if (h0 < p.hq) warp_merge_heads<2>(p, blockIdx.x, h0, threadIdx.x & 31);
   if (p.trace != nullptr && (threadIdx.x & 31) == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -182,7 +182,7 @@ cudaError_t launch_generic(const AttnParams& p, cudaStream_t st) {
 cudaError_t launch_merge(const AttnParams& p, cudaStream_t st, bool pdl) {
   if (p.n_merge <= 0) return cudaSuccess;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(p.n_merge, (p.hq + 7) / 8);
+  cfg.gridDim = dim3(p.n_merge, (p.hq + 15) / 16);   // 8 warps x 2 heads per block
   cfg.blockDim = dim3(256);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];

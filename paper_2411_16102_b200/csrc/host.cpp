@@ -488,6 +488,11 @@ int build_plan(blend_tree* t) {
       }
     }
   }
+  // A SEPARATE item's rows may come in any order (every row carries its own position
+  // and partmap slot): ascending q rows make the users' tokens consecutive wherever the
+  // caller keeps them together, so the dense kernel loads such Q tiles with whole TMA
+  // boxes instead of one box per token.
+  for (auto& it : items) std::sort(it.toks.begin(), it.toks.end());
   for (int32_t k = 0; k < R; ++k) {
     int32_t r = t->dfs_order[k];
     Item it;
