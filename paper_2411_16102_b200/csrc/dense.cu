@@ -35,6 +35,10 @@
 
 namespace blend {
 
+#ifndef BLEND_TRACE_BLOCKS
+#define BLEND_TRACE_BLOCKS 0   // 1: per-block S / P stamps in the diagnostics trace (costs issue slots)
+#endif
+
 constexpr int DN_THREADS = 384;
 constexpr int DN_KB = 64;                // keys per block (UMMA N of QK^T, K of PV)
 constexpr int DN_QCHUNK = 128 * 128;     // Q: 128 rows x 128 B (one 64-column chunk)
@@ -356,9 +360,12 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
     };
     auto load_meta = [&](const Unit& un, int j) {
 #pragma unroll
-      for (int i = 0; i < EPB; ++i) {
+      for (int i = 0; i < EPB; ++i) {   // one 8-byte load per entry, no branch (padding: count 0)
         const int e = un.entry_begin + j * EPB + i;
-        enext[i] = e < un.entry_end ? make_int2(p.entries[e].pos0, p.entries[e].count) : make_int2(0, 0);
+        const int ec = e < un.entry_end ? e : un.entry_end - 1;
+        int2 v = *reinterpret_cast<const int2*>(&p.entries[ec].pos0);
+        if (e >= un.entry_end) v.y = 0;
+        enext[i] = v;
       }
     };
     for (int ui = blockIdx.x; ui < p.n_units; ui += gridDim.x) {
@@ -404,7 +411,9 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         }
         ptx::mbar_wait(&s_full[t * 2 + buf], (buf ? scnt1++ : scnt0++) & 1);   // per-buffer completion count
         ptx::tc_fence_after();
+#if BLEND_TRACE_BLOCKS
         if (threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 8 + 2 * j);
+#endif
         float sv[DN_KB];
         ptx::tmem_ld32(tmem + lane_base + col_s, reinterpret_cast<uint32_t*>(sv));
         ptx::tmem_ld32(tmem + lane_base + col_s + 32, reinterpret_cast<uint32_t*>(sv + 32));
@@ -480,7 +489,9 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&p_full[t * 2 + buf]);
+#if BLEND_TRACE_BLOCKS
         if (threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 9 + 2 * j);
+#endif
       }
       if (threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 4);
       // ---- epilogue: PV of the unit's last block done (MMAs complete in issue order, so
