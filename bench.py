@@ -223,7 +223,9 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": w.name},
+            "config": {"workload": w.name, "requests": w.n_req, "query_tokens": int(w.sum_q),
+                       "heads": f"{w.num_q_heads}/{w.num_kv_heads}x{w.head_dim}", "page_size": w.page_size,
+                       "parallelism": "host cores (fp64 oracle)"},
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle",
                              "sample": sample_desc},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
