@@ -422,6 +422,46 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
 #pragma unroll
           for (int k = 0; k < DN_KB; ++k) sv[k] = (k % BOX) < vis[k / BOX] ? sv[k] : -INFINITY;
         }
+        // P = exp2(s*scale - m) on packed fp32 pairs (FFMA2/FADD2): 3 of every 4 pairs on the
+        // MUFU pipe, 1 of 4 as a polynomial on the FMA pipe; bf16 pairs -> the first 32 TMEM
+        // columns of this S buffer.
+        uint32_t pk[DN_KB / 2];
+        float lsum = 0.f;
+        auto exps = [&](float m_use) {
+          const uint64_t sc2 = ptx::f2pack(p.scale_log2, p.scale_log2), nm2 = ptx::f2pack(-m_use, -m_use);
+          uint64_t ls2[2] = {ptx::f2pack(0.f, 0.f), ptx::f2pack(0.f, 0.f)};
+#pragma unroll
+          for (int k = 0; k < DN_KB / 2; ++k) {
+            const uint64_t x2 = ptx::ffma2(ptx::f2pack(sv[2 * k], sv[2 * k + 1]), sc2, nm2);
+            uint64_t p2;
+            if ((POLY >> (k & 15)) & 1u) {
+              p2 = ptx::exp2_poly2(x2);
+            } else {
+              float x0, x1;
+              ptx::f2unpack(x2, x0, x1);
+              p2 = ptx::f2pack(ptx::ex2(x0), ptx::ex2(x1));
+            }
+            ls2[k & 1] = ptx::fadd2(ls2[k & 1], p2);
+            float p0, p1;
+            ptx::f2unpack(p2, p0, p1);
+            pk[k] = ptx::pack_bf16(p0, p1);
+          }
+          float ls[4];
+          ptx::f2unpack(ls2[0], ls[0], ls[1]);
+          ptx::f2unpack(ls2[1], ls[2], ls[3]);
+          lsum = (ls[0] + ls[1]) + (ls[2] + ls[3]);
+        };
+        // Fast path: exponentiate against the running reference m_ref without the block
+        // max.  Lazy rescaling keeps m_ref unless the max grows by more than 2^8, i.e. unless
+        // some p > 2^8; the block sum bounds every p, so lsum <= 2^8 proves this block keeps
+        // m_ref and P is exactly what the max-first order computes.  Otherwise (and on a
+        // unit's first block) the warp takes the max-first path below.
+        bool slow = __any_sync(0xffffffffu, m_ref == -INFINITY);
+        if (!slow) {
+          exps(m_ref);
+          slow = __any_sync(0xffffffffu, !(lsum <= 256.f));
+        }
+        if (slow) {
         float mxv[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) mxv[i] = sv[i];
@@ -453,38 +493,11 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
           l *= ptx::ex2(m_ref - mx2);   // m_ref = -inf -> 0
           m_ref = mx2;
         }
-        const float m_use = m_ref == -INFINITY ? 0.f : m_ref;
-        // P = exp2(s*scale - m) on packed fp32 pairs (FFMA2/FADD2): 3 of every 4 pairs on the
-        // MUFU pipe, 1 of 4 as a polynomial on the FMA pipe; bf16 pairs -> the first 32 TMEM
-        // columns of this S buffer
-        const uint64_t sc2 = ptx::f2pack(p.scale_log2, p.scale_log2), nm2 = ptx::f2pack(-m_use, -m_use);
-        uint64_t ls2[2] = {ptx::f2pack(0.f, 0.f), ptx::f2pack(0.f, 0.f)};
-#pragma unroll
-        for (int c = 0; c < DN_KB / 32; ++c) {
-          uint32_t pk[16];
-#pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            const int key = c * 32 + 2 * k;
-            const uint64_t x2 = ptx::ffma2(ptx::f2pack(sv[key], sv[key + 1]), sc2, nm2);
-            uint64_t p2;
-            if ((POLY >> k) & 1u) {
-              p2 = ptx::exp2_poly2(x2);
-            } else {
-              float x0, x1;
-              ptx::f2unpack(x2, x0, x1);
-              p2 = ptx::f2pack(ptx::ex2(x0), ptx::ex2(x1));
-            }
-            ls2[k & 1] = ptx::fadd2(ls2[k & 1], p2);
-            float p0, p1;
-            ptx::f2unpack(p2, p0, p1);
-            pk[k] = ptx::pack_bf16(p0, p1);
-          }
-          ptx::tmem_st16(tmem + lane_base + col_s + c * 16, pk);
+          exps(m_ref == -INFINITY ? 0.f : m_ref);
         }
-        float ls[4];
-        ptx::f2unpack(ls2[0], ls[0], ls[1]);
-        ptx::f2unpack(ls2[1], ls[2], ls[3]);
-        l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+#pragma unroll
+        for (int c = 0; c < DN_KB / 32; ++c) ptx::tmem_st16(tmem + lane_base + col_s + c * 16, pk + 16 * c);
+        l += lsum;
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
         __syncwarp();
