@@ -25,6 +25,10 @@
 
 namespace blend {
 
+#ifndef BLEND_TRACE_STAGES
+#define BLEND_TRACE_STAGES 0   // 1: per-stage stamps (stages 4..11 of ring 0) in the diagnostics trace
+#endif
+
 constexpr int SW_WARPS = 4;                  // consumer warps = rings = producer warps
 constexpr int SW_THREADS = 32 * (2 * SW_WARPS);
 constexpr int SW_STAGES = 3;
@@ -152,6 +156,9 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
           for (int h = 0; h * SW_KEYS < count; ++h, ++it) {
             const uint32_t s = it % SW_STAGES, ph = (it / SW_STAGES) & 1;
             ptx::mbar_wait(&rempty[s], ph ^ 1);
+#if BLEND_TRACE_STAGES
+            if (w == 0 && it >= 4 && it < 12) trace_stamp_s(p, 52 + (it - 4));
+#endif
             const int left = count - h * SW_KEYS;
             const int rows = ((left < SW_KEYS ? left : SW_KEYS) + 15) & ~15;
             const int32_t y = (cur.x * p.hkv + u_cur.kvh) * p.ps + cur.y + h * SW_KEYS;
@@ -310,6 +317,9 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
         const int nvalid = en_count - kbase;           // >= 1
         ptx::mbar_wait(&wfull[s], ph);
         if (warp == 0 && lane == 0 && k == 0 && h == 0) trace_stamp_s(p, 3 + 4 * tu);
+#if BLEND_TRACE_STAGES
+        if (warp == 0 && lane == 0 && it >= 4 && it < 12) trace_stamp_s(p, 36 + (it - 4));
+#endif
         const uint32_t kst = ptx::smem_u32(ring + s * L.stage_stride);
         const uint32_t vst = kst + CH * SW_CHUNK;
         const int ntv = nvalid >= SW_KEYS ? 4 : (nvalid + 7) / 8;   // n-tiles holding valid keys
@@ -393,6 +403,9 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
         }
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&wempty[s]);
+#if BLEND_TRACE_STAGES
+        if (warp == 0 && lane == 0 && it >= 4 && it < 12) trace_stamp_s(p, 44 + (it - 4));
+#endif
         if (q_pending) {
           issue_q(pre, buf ^ 1);
           q_pending = false;

@@ -41,7 +41,11 @@ for u in range(14):
     st, fd, ke, en = (np.nanmedian(rel[:, c]) for c in cols)
     n = int(np.sum(~np.isnan(rel[:, cols[0]])))
     print(f"  unit {u}: start {st:7.2f} data {fd:7.2f} kv_end {ke:7.2f} end {en:7.2f}  ({n} CTAs)")
-last = np.nanmax(rel[:, 2:38], axis=1)
+if not np.all(np.isnan(rel[:, 36])):
+    print("  stages 4..11 (ring 0): TMA issue", [round(float(np.nanmedian(rel[:, 52 + k])), 2) for k in range(8)])
+    print("                         data      ", [round(float(np.nanmedian(rel[:, 36 + k])), 2) for k in range(8)])
+    print("                         freed     ", [round(float(np.nanmedian(rel[:, 44 + k])), 2) for k in range(8)])
+last = np.nanmax(rel[:, 2:30], axis=1)
 d6 = t[:148, 6][t[:148, 6] > 0]
 if len(d6):
     print(f"  dense CTA exit: median {np.median((d6 - t0) / 1e3):.2f} max {np.max((d6 - t0) / 1e3):.2f} us")
