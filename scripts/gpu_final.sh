@@ -8,7 +8,7 @@ python -m paper_2411_16102_b200.compile > /dev/null 2>&1 || { echo build failed;
 timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
 timeout 300 python __graft_entry__.py smoke 2>&1 | tail -4
 timeout 600 python bench.py > $OUT/bench_default.json 2> $OUT/bench_default.err; tail -c 400 $OUT/bench_default.json
-timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_reference.json 2>&1; tail -c 300 $OUT/bench_reference.json
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $OUT/bench_reference.json 2>&1; tail -c 300 $OUT/bench_reference.json
 for W in c3 c4 c5; do timeout 300 python bench.py --workload $W --steps 10 --warmup 3 --no-cpu-baseline 2>&1 | tail -1 > $OUT/bench_$W.json; done
 for W in c2 c4; do
 timeout 600 $NCU --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_${W}.csv \
