@@ -112,11 +112,9 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
       // Unit pipeline, two deep: while unit k's stages are issued, unit k+1 is known
       // (struct loaded, announced, first entry requested) and unit k+2's index is being
       // fetched from the counter, so no dependent global load sits between two units.
-      // The first SW_STATIC units of every ring are assigned statically (round-robin over
-      // the longest-first order); the rest are handed out by the counter.  Measured on
-      // B200: while the overlapped dense grid runs, a same-address atomicAdd by the
-      // streaming producers can take ~10 us to return, so the counter stays off the
-      // start-up path.
+      // Units come from the counter (greedy LPT over the longest-first order); the first
+      // SW_STATIC per ring may instead be assigned round-robin (0 measured best: rings on
+      // SMs freed late by the overlapped dense grid should take fewer units).
       const int R = (int)gridDim.x * SW_WARPS, ring_id = (int)blockIdx.x * SW_WARPS + w;
       const int nstat = n / R < SW_STATIC ? n / R : SW_STATIC;
       int k_next = 0;   // units of this ring handed out so far
