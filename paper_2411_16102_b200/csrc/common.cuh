@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include "internal.h"
+#include "ptx.cuh"
 
 namespace blend {
 
@@ -144,14 +145,13 @@ __device__ __forceinline__ void fused_merge_store(const AttnParams& p, int32_t t
 template <int NH>
 __device__ __forceinline__ void warp_merge_heads(const AttnParams& p, int m, int h0, int lane) {
   // NH q heads of merge list m per warp: both heads' loads of a chunk are in flight
-  // together (half the warps of one head per warp, so the grid fits one wave)
+  // together (half the warps of one head per warp, so the grid fits one wave).  32-bit
+  // index math, MUFU ex2 / lg2 / rcp, and one vector store per lane and head.
   const int token = p.merge_tok[m];
   const int s0 = p.merge_off[m], s1 = p.merge_off[m + 1];
-  const int D = p.d;
+  const int D = p.d, hq = p.hq;
   const int vec = D / 32;          // 2 or 4 elements per lane
   const int e0 = lane * vec;
-  // One pass in chunks of MCH sources: every load of a chunk is issued before any is
-  // used (rows -> lse -> o are the only dependent steps), then an online rescale.
   constexpr int MCH = 2;
   float mx[NH], tot[NH], acc[NH][4];
 #pragma unroll
@@ -165,22 +165,18 @@ __device__ __forceinline__ void warp_merge_heads(const AttnParams& p, int m, int
     float4 v[NH][MCH];
 #pragma unroll
     for (int j = 0; j < NH; ++j) {
-      const int h = h0 + j < p.hq ? h0 + j : h0;
+      const int h = h0 + j < hq ? h0 + j : h0;
 #pragma unroll
       for (int i = 0; i < MCH; ++i) {
-        const int64_t row = c0 + i;   // unfused: entry s is partial row s
         const bool ok = c0 + i < s1;
-        l[j][i] = ok ? __ldcg(p.ws_lse + row * p.hq + h) : -INFINITY;
-        v[j][i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (ok) {
-          const float* src = p.ws_o + (row * p.hq + h) * D + e0;
-          if (vec == 4) {
-            v[j][i] = __ldcg(reinterpret_cast<const float4*>(src));
-          } else {
-            const float2 t = __ldcg(reinterpret_cast<const float2*>(src));
-            v[j][i].x = t.x;
-            v[j][i].y = t.y;
-          }
+        const int r = (ok ? c0 + i : c0) * hq + h;   // unfused: entry s is partial row s
+        l[j][i] = ok ? __ldcg(p.ws_lse + r) : -INFINITY;
+        const float* src = p.ws_o + (size_t)r * D + e0;
+        if (vec == 4) {
+          v[j][i] = __ldcg(reinterpret_cast<const float4*>(src));
+        } else {
+          const float2 t = __ldcg(reinterpret_cast<const float2*>(src));
+          v[j][i] = make_float4(t.x, t.y, 0.f, 0.f);
         }
       }
     }
@@ -190,13 +186,13 @@ __device__ __forceinline__ void warp_merge_heads(const AttnParams& p, int m, int
 #pragma unroll
       for (int i = 0; i < MCH; ++i) cm = fmaxf(cm, l[j][i]);
       if (cm == -INFINITY) continue;
-      const float a = exp2f(mx[j] - cm);      // mx = -inf on the first live chunk -> 0
+      const float a = ptx::ex2(mx[j] - cm);      // mx = -inf on the first live chunk -> 0
       tot[j] *= a;
 #pragma unroll
       for (int k = 0; k < 4; ++k) acc[j][k] *= a;
 #pragma unroll
       for (int i = 0; i < MCH; ++i) {
-        const float w = exp2f(l[j][i] - cm);  // l = -inf (absent source) -> 0
+        const float w = ptx::ex2(l[j][i] - cm);  // l = -inf (absent source) -> 0
         tot[j] += w;
         acc[j][0] = fmaf(w, v[j][i].x, acc[j][0]);
         acc[j][1] = fmaf(w, v[j][i].y, acc[j][1]);
@@ -209,11 +205,24 @@ __device__ __forceinline__ void warp_merge_heads(const AttnParams& p, int m, int
 #pragma unroll
   for (int j = 0; j < NH; ++j) {
     const int h = h0 + j;
-    if (h >= p.hq) break;
-    const float inv = tot[j] > 0.f ? 1.f / tot[j] : 0.f;
-    const int64_t ob = ((int64_t)token * p.hq + h) * D + e0;
-    for (int k = 0; k < vec; ++k) st_elem(p.out, ob + k, acc[j][k] * inv, p.kv_f32);
-    if (lane == 0) p.lse[(int64_t)token * p.hq + h] = mx[j] != -INFINITY ? (mx[j] + log2f(tot[j])) * kLn2 : -INFINITY;
+    if (h >= hq) break;
+    const float inv = tot[j] > 0.f ? ptx::rcp(tot[j]) : 0.f;
+    const int64_t ob = (int64_t)(token * hq + h) * D + e0;   // out can exceed 2^31 elements (C4)
+    if (p.kv_f32) {
+      float* dst = reinterpret_cast<float*>(p.out) + ob;
+      if (vec == 4)
+        *reinterpret_cast<float4*>(dst) = make_float4(acc[j][0] * inv, acc[j][1] * inv, acc[j][2] * inv, acc[j][3] * inv);
+      else
+        *reinterpret_cast<float2*>(dst) = make_float2(acc[j][0] * inv, acc[j][1] * inv);
+    } else {
+      __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.out) + ob;
+      const uint32_t b01 = ptx::pack_bf16(acc[j][0] * inv, acc[j][1] * inv);
+      if (vec == 4)
+        *reinterpret_cast<uint2*>(dst) = make_uint2(b01, ptx::pack_bf16(acc[j][2] * inv, acc[j][3] * inv));
+      else
+        *reinterpret_cast<uint32_t*>(dst) = b01;
+    }
+    if (lane == 0) p.lse[token * hq + h] = mx[j] != -INFINITY ? (mx[j] + ptx::lg2(tot[j])) * kLn2 : -INFINITY;
   }
 }
 
