@@ -29,9 +29,13 @@ namespace blend {
 #define BLEND_TRACE_STAGES 0   // 1: per-stage stamps (stages 4..11 of ring 0) in the diagnostics trace
 #endif
 
-constexpr int SW_WARPS = 4;                  // consumer warps = rings = producer warps
+#ifndef SW_WARPS_CFG
+#define SW_WARPS_CFG 4
+#define SW_STAGES_CFG 3
+#endif
+constexpr int SW_WARPS = SW_WARPS_CFG;                  // consumer warps = rings = producer warps
 constexpr int SW_THREADS = 32 * (2 * SW_WARPS);
-constexpr int SW_STAGES = 3;
+constexpr int SW_STAGES = SW_STAGES_CFG;
 constexpr int SW_STATIC = 0;                 // statically assigned units per ring (0: all dynamic, measured best)
 constexpr int SW_KEYS = 32;                  // keys per stage (half a 64-slot entry)
 constexpr int SW_CHUNK = SW_KEYS * 128;      // 32 rows x 128 B

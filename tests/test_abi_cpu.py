@@ -179,3 +179,12 @@ def test_plan_simulation_mixed_sep_rows(seed):
                         max_q=64)
     for kw in (dict(), dict(force_class=1, min_sep_len=0), dict(rows_min=16, min_sep_len=0)):
         _check_sim(w, **kw)
+
+
+@pytest.mark.parametrize("hq,hkv,d,ps", [(6, 3, 128, 64), (12, 4, 64, 32), (8, 1, 128, 128), (10, 2, 128, 16)])
+def test_plan_simulation_group_sizes(hq, hkv, d, ps):
+    """Planner + plan image for GQA groups 2, 3, 8, 5 (tiles that split tokens when
+    g does not divide 128) reproduce the oracle in fp64 simulation."""
+    w = random_workload(100 + hq, hq=hq, hkv=hkv, d=d, kv_dtype="f32", page_size=ps, max_seg=300, n_req=24)
+    for kw in (dict(), dict(force_class=1, min_sep_len=0), dict(rows_min=8, min_sep_len=0)):
+        _check_sim(w, **kw)

@@ -251,3 +251,17 @@ def test_arrival_merge_counters(kw):
     db.run()                                   # merge kernel: same attention within tolerance
     torch.cuda.synchronize()
     _cmp(w, db)
+
+
+@pytest.mark.parametrize("hq,hkv,d,ps", [(6, 3, 128, 64), (12, 4, 64, 32), (8, 1, 128, 128), (10, 2, 128, 16)])
+def test_group_sizes_bf16(hq, hkv, d, ps):
+    """GQA group sizes 2, 3, 8, 5: g = 3 and 5 do not divide a 128-row tile (dense units
+    gather Q rows with cp.async, tiles split tokens), g = 2 / 8 use the TMA Q boxes;
+    page sizes 16..128 exercise the multi-entry 64-key blocks."""
+    w = random_workload(100 + hq, hq=hq, hkv=hkv, d=d, kv_dtype="bf16", page_size=ps, max_seg=300,
+                        n_req=24)
+    for kw in (dict(), dict(force_class=1, min_sep_len=0), dict(rows_min=8, min_sep_len=0)):
+        db = device_batch(w, tree_kw=kw)
+        db.run()
+        torch.cuda.synchronize()
+        _cmp(w, db)
