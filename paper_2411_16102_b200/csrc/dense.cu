@@ -35,6 +35,9 @@
 
 namespace blend {
 
+#ifndef BLEND_TRACE_UNITS
+#define BLEND_TRACE_UNITS 0    // 1: per-unit start / epilogue-end stamps (first 10 units of each CTA)
+#endif
 #ifndef BLEND_TRACE_BLOCKS
 #define BLEND_TRACE_BLOCKS 0   // 1: per-block S / P stamps in the diagnostics trace (costs issue slots)
 #endif
@@ -373,6 +376,10 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       const int nb = (u.entry_end - u.entry_begin + EPB - 1) / EPB;
       if (t == 1 && u.n_rows <= 128) continue;       // tile B idle for this unit
       const int row = 128 * t + r;                    // row within the unit
+#if BLEND_TRACE_UNITS
+      const int uk = (ui - (int)blockIdx.x) / (int)gridDim.x;   // this CTA's k-th unit
+      if (threadIdx.x == 128 && uk < 10) trace_stamp(p, 20 + 2 * uk);
+#endif
       int32_t pos = INT32_MIN, token = 0, head = 0, tgt = PM_SKIP;
       if (row < u.n_rows) {
         // a TMA-loaded unit's tokens are consecutive from dqtok: no item_tokens round trip
@@ -384,6 +391,11 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         pos = p.tok_pos[token];
       }
       float m_ref = -INFINITY, l = 0.f;
+      const bool row_ok = row < u.n_rows;
+      // a warp whose 32 rows are all padding (tile B of a 129..223-row unit) skips the
+      // softmax: its P rows only feed its own (never stored) O rows, so they may hold
+      // anything; it keeps the barrier protocol
+      const bool warp_pad = __all_sync(0xffffffffu, !row_ok);
       int2 am = make_int2(-1, 0);                     // {merge list, sources} of a partial row
       load_meta(u, 0);
       for (int j = 0; j < nb; ++j, ++sb) {
@@ -414,6 +426,11 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
 #if BLEND_TRACE_BLOCKS
         if (threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 8 + 2 * j);
 #endif
+        if (warp_pad) {
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&p_full[t * 2 + buf]);
+          continue;
+        }
         float sv[DN_KB];
         ptx::tmem_ld32(tmem + lane_base + col_s, reinterpret_cast<uint32_t*>(sv));
         ptx::tmem_ld32(tmem + lane_base + col_s + 32, reinterpret_cast<uint32_t*>(sv + 32));
@@ -456,11 +473,16 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         // some p > 2^8; the block sum bounds every p, so lsum <= 2^8 proves this block keeps
         // m_ref and P is exactly what the max-first order computes.  Otherwise (and on a
         // unit's first block) the warp takes the max-first path below.
-        bool slow = __any_sync(0xffffffffu, m_ref == -INFINITY);
+        bool slow = __any_sync(0xffffffffu, row_ok && m_ref == -INFINITY);
         if (!slow) {
-          exps(m_ref);
+          exps(m_ref == -INFINITY ? 0.f : m_ref);   // -inf: a padding row (all scores masked)
           slow = __any_sync(0xffffffffu, !(lsum <= 256.f));
         }
+#if BLEND_TRACE_UNITS
+        if (p.trace != nullptr && lane == 0) {   // diagnostics: blocks per path (fast / slow)
+          atomicAdd(p.trace + 296 * 64 + 8 + (slow ? 1 : 0), 1ull);
+        }
+#endif
         if (slow) {
         float mxv[8];
 #pragma unroll
@@ -583,6 +605,9 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       }
       ptx::tc_fence_before();
       if (threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 5);
+#if BLEND_TRACE_UNITS
+      if (threadIdx.x == 128 && uk < 10) trace_stamp(p, 21 + 2 * uk);
+#endif
     }
     if (p.arrive != nullptr) settle();
   }
