@@ -35,6 +35,10 @@
 
 namespace blend {
 
+#ifndef DN_NSTAGE128
+#define DN_NSTAGE128 4     // K/V ring stages at D = 128 (64 keys each)
+#define DN_STAGED_EPI 1    // epilogue through the smem staging tile (else per-thread row stores)
+#endif
 #ifndef BLEND_TRACE_UNITS
 #define BLEND_TRACE_UNITS 0    // 1: per-unit start / epilogue-end stamps (first 10 units of each CTA)
 #endif
@@ -61,10 +65,10 @@ __host__ __device__ inline DenseSmem dense_layout(int D) {
   L.q1 = CH * DN_QCHUNK;
   L.stage0 = 2 * CH * DN_QCHUNK;
   L.stage_stride = 2 * CH * DN_KCHUNK;   // K chunks then V chunks
-  L.nstage = D == 128 ? 4 : 8;
+  L.nstage = D == 128 ? DN_NSTAGE128 : 8;
   L.bar = L.stage0 + L.nstage * L.stage_stride;
   L.stg = L.bar + 512;                    // epilogue staging: per softmax warp 32 rows x 128 B
-  L.total = L.stg + 8 * 4096;
+  L.total = L.stg + (DN_STAGED_EPI ? 8 * 4096 : 0);
   return L;
 }
 
@@ -545,11 +549,36 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       // bank conflicts), so that every global store instruction writes whole 128-B row
       // segments (4 rows per instruction) instead of 32 scattered 16-B pieces.
       // Row kinds: 2 = fp32 partial row, 1 = bf16 output row (DIRECT), 0 = nothing.
-      {
+      if (!DN_STAGED_EPI) {
+        // each thread writes its own row (16-B stores)
+#pragma unroll 1
+        for (int hh = 0; hh < D / 64; ++hh) {
+          uint32_t ov2[64];
+          ptx::tmem_ld32(tmem + lane_base + col_o + hh * 64, ov2);
+          ptx::tmem_ld32(tmem + lane_base + col_o + hh * 64 + 32, ov2 + 32);
+          ptx::tmem_wait_ld();
+          if (tgt == PM_DIRECT) {
+            char* dst = reinterpret_cast<char*>(p.out) + (((int64_t)token * p.hq + head) * D + hh * 64) * 2;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              ptx::stg128u(dst + u * 16, make_uint4(
+                  ptx::pack_bf16(__uint_as_float(ov2[8 * u]) * inv, __uint_as_float(ov2[8 * u + 1]) * inv),
+                  ptx::pack_bf16(__uint_as_float(ov2[8 * u + 2]) * inv, __uint_as_float(ov2[8 * u + 3]) * inv),
+                  ptx::pack_bf16(__uint_as_float(ov2[8 * u + 4]) * inv, __uint_as_float(ov2[8 * u + 5]) * inv),
+                  ptx::pack_bf16(__uint_as_float(ov2[8 * u + 6]) * inv, __uint_as_float(ov2[8 * u + 7]) * inv)));
+          } else if (tgt >= 0) {
+            float* dst = p.ws_o + ((int64_t)tgt * p.hq + head) * D + hh * 64;
+#pragma unroll
+            for (int u = 0; u < 16; ++u)
+              ptx::stg128(dst + 4 * u, make_float4(__uint_as_float(ov2[4 * u]) * inv, __uint_as_float(ov2[4 * u + 1]) * inv,
+                                                   __uint_as_float(ov2[4 * u + 2]) * inv, __uint_as_float(ov2[4 * u + 3]) * inv));
+          }
+        }
+      } else {
         const int kind = tgt == PM_DIRECT ? 1 : (tgt >= 0 ? 2 : 0);
         char* rowp = kind == 1 ? reinterpret_cast<char*>(p.out) + ((int64_t)token * p.hq + head) * D * 2
                    : kind == 2 ? reinterpret_cast<char*>(p.ws_o + ((int64_t)tgt * p.hq + head) * D) : nullptr;
-        const uint32_t stg = ptx::smem_u32(smem + L.stg + (warp - 4) * 4096);
+        const uint32_t stg = ptx::smem_u32(smem + L.stg + (DN_STAGED_EPI ? (warp - 4) * 4096 : 0));
         const int k8 = lane & 7;
         char* rp[8];
         int rk[8];
