@@ -265,3 +265,36 @@ def test_group_sizes_bf16(hq, hkv, d, ps):
         db.run()
         torch.cuda.synchronize()
         _cmp(w, db)
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_sharded_equals_single_gpu(G):
+    """§8(e) invariant "G-GPU == 1-GPU" on one device: the bench's N-GPU recipe (N
+    independent C2 copies), sharded by blend_shard into G subtree shards, each shard
+    planned and run on its own; re-assembled in global request order the outputs equal
+    the unsharded run's within the bf16 tolerance (different plans, so not bitwise) and
+    the oracle on a sample of requests."""
+    from harness.run import build_tree, subset
+    gw = W.replicate(lambda seed: W.c2_mmlu_decode(n_req=48, seed=seed), G, 2)
+    dbg = device_batch(gw)
+    dbg.run()
+    torch.cuda.synchronize()
+    full = dbg.out.float().cpu().numpy()
+    req_shard, _ = build_tree(gw).shard(G)
+    qo = np.concatenate([[0], np.cumsum(gw.q_len)])
+    seen = np.zeros(gw.n_req, dtype=bool)
+    for g in range(G):
+        mine = np.nonzero(req_shard == g)[0]
+        assert len(mine) > 0
+        ws = subset(gw, mine)
+        db = device_batch(ws)
+        db.run()
+        torch.cuda.synchronize()
+        o = db.out.float().cpu().numpy()
+        qs = np.concatenate([[0], np.cumsum(ws.q_len)])
+        for i, r in enumerate(mine):
+            a, b = full[qo[r]:qo[r + 1]], o[qs[i]:qs[i + 1]]
+            assert np.max(np.abs(a - b)) <= 2e-2, (g, int(r))
+            seen[r] = True
+        _cmp(ws, db, requests=list(range(0, ws.n_req, max(1, ws.n_req // 6))))
+    assert seen.all(), "every request in exactly one shard"
