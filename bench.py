@@ -445,8 +445,9 @@ def run_ours(args):
             "roofline": roof,
             "cpu_baseline": cpu,
             "passes_ms": {"dense": md, "stream": mst, "merge": mm, "serialized_step": mser,
-                          "note": "per-pass times from K extra steps run with BLEND_SERIALIZE; the timed "
-                                  "steps overlap the dense and streaming passes (PDL)"},
+                          "note": "per-pass times from K extra steps run with BLEND_SERIALIZE (dense grid on "
+                                  "every SM); the timed steps overlap the dense and streaming passes (PDL), "
+                                  "with the dense grid capped by the planner when both passes are large"},
             "work": {"F_alg": F, "B_alg": Bytes, "kv_bytes": KVb, **pw,
                      "whole_step_roofline_frac_measured": max(F / (load_peaks()["bf16_tflops"] * 1e12),
                                                               Bytes / (load_peaks()["hbm_gbs"] * 1e9)) / (ms * 1e-3)},

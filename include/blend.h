@@ -176,7 +176,7 @@ typedef struct {
   int64_t off[16];           /* section offsets inside dev                        */
   int64_t count[16];         /* section element counts                            */
   int32_t num_q_heads, num_kv_heads, head_dim, kv_dtype, page_size;
-  int32_t reserved;
+  int32_t reserved;          /* planner's dense-pass grid cap (0: one CTA per SM)     */
 } blend_plan;
 
 /* Copy the plan (host, inside the tree) into dev_buf (device, >= blend_plan_bytes)

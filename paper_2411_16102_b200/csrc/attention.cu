@@ -14,6 +14,7 @@ extern "C" int blend_internal_tree_dims(const blend_tree* t, int32_t* dims);
 extern "C" int64_t blend_internal_partial_rows(const blend_tree* t);
 extern "C" int64_t blend_internal_stream_entries(const blend_tree* t);
 extern "C" int64_t blend_internal_merge_unfused(const blend_tree* t);
+extern "C" int32_t blend_internal_dense_ctas(const blend_tree* t);
 
 namespace blend {
 cudaError_t launch_generic(const AttnParams& p, cudaStream_t st);
@@ -70,7 +71,7 @@ extern "C" int blend_plan_upload(const blend_tree* tree, void* dev_buf, size_t b
   plan->head_dim = dims[2];
   plan->kv_dtype = dims[3];
   plan->page_size = dims[4];
-  plan->reserved = 0;
+  plan->reserved = blend_internal_dense_ctas(tree);
   return BLEND_OK;
 }
 
@@ -149,6 +150,7 @@ extern "C" int blend_attention(const blend_attn_args* a, void* stream) {
   int32_t* arrive = arrival ? (int32_t*)((char*)a->workspace + o_bytes + lse_bytes + 256) : nullptr;
   pd.arrive = arrive;
   pd.trace = g_trace;
+  pd.dense_ctas = overlap ? pl.reserved : 0;   // the cap only makes room for the overlapped streaming grid
   pd.sched = stream_dyn && dense_tc ? p.sched : nullptr;
   if (stream_dyn && !dense_tc) {
     e = cudaMemsetAsync(p.sched, 0, sizeof(int32_t), st);

@@ -41,6 +41,7 @@ struct AttnParams {
   int32_t* arrive;       // arrival counters [partial row][Hq] (workspace; NULL: the merge kernel merges)
   const int32_t* dqtok;  // dense units: first token when the unit's tokens are consecutive, else -1
   int32_t n_tokens;      // query tokens (rows of q / out)
+  int32_t dense_ctas;    // dense grid cap from the planner (0: one CTA per SM)
   unsigned long long* trace;   // diagnostics only (blend_internal_set_trace): [CTA][64] globaltimer stamps
 };
 

@@ -674,7 +674,8 @@ static cudaError_t launch_dense_db(const AttnParams& p, int64_t n_cache_pages, c
   const size_t smem = dense_layout(D).total + 1024;
   e = set_smem_once((const void*)dense_kernel<D, BOX>, smem);
   if (e != cudaSuccess) return e;
-  const int grid = p.n_units < num_sms_cached() ? p.n_units : num_sms_cached();
+  int grid = p.n_units < num_sms_cached() ? p.n_units : num_sms_cached();
+  if (p.dense_ctas > 0 && grid > p.dense_ctas) grid = p.dense_ctas;   // planner: SMs left to streaming
   dense_kernel<D, BOX><<<grid, DN_THREADS, smem, st>>>(tk, tv, tq, tq1, p);
   return cudaPeekAtLastError();
 }

@@ -102,6 +102,7 @@ struct blend_tree {
   int64_t n_partial_rows = 0;
   int64_t stream_entries = 0;   // sum over stream units of their entry counts (launch heuristic)
   int32_t n_merge_unfused = 0;  // merge lists [0, n) are merged by the merge kernel
+  int32_t dense_ctas = 0;       // dense-pass grid cap (0: one CTA per SM), set by the planner
 };
 
 namespace {
@@ -544,6 +545,17 @@ int build_plan(blend_tree* t) {
   // overlap f = max, §2.4) and split its items until that share is filled.
   // Rates are planning constants measured on B200 for the two kernels (~250 TFLOP/s for
   // the short dense units this split targets, ~6 TB/s streaming).
+  // When the dense pass alone would fill the GPU and both passes are substantial, cap
+  // its grid so the overlapped streaming grid starts on the remaining SMs at once
+  // (measured on B200: C4 -2 %, C5 -3 % with caps near these shares; the share moves
+  // from 0.4 toward 1 as the dense estimate dominates).  Rates: ~690 TFLOP/s dense,
+  // ~6.9 TB/s streaming (round-1 measurements).
+  t->dense_ctas = 0;
+  if (base_d >= num_sms && flops_d > 0.0 && bytes_s > 0.0) {
+    const double td = flops_d / 690e12, ts = bytes_s / 6.9e12;
+    if (td > 0.2 * (td + ts) && ts > 0.2 * (td + ts))
+      t->dense_ctas = (int32_t)((0.4 + 0.6 * td / (td + ts)) * num_sms + 0.5);
+  }
   int64_t dsplit = 1;
   if (a.dense_split > 0) dsplit = a.dense_split;
   else if (base_d > 0 && base_d < num_sms) {
@@ -1052,6 +1064,7 @@ int blend_internal_fail(int status, const char* msg) { return fail(status, "%s",
 int64_t blend_internal_partial_rows(const blend_tree* t) { return t ? t->n_partial_rows : 0; }
 int64_t blend_internal_stream_entries(const blend_tree* t) { return t ? t->stream_entries : 0; }
 int64_t blend_internal_merge_unfused(const blend_tree* t) { return t ? t->n_merge_unfused : 0; }
+int32_t blend_internal_dense_ctas(const blend_tree* t) { return t ? t->dense_ctas : 0; }
 
 int blend_internal_tree_dims(const blend_tree* t, int32_t* dims) {
   if (!t) return fail(BLEND_EINVAL, "tree is NULL");
