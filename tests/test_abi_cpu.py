@@ -188,3 +188,17 @@ def test_plan_simulation_group_sizes(hq, hkv, d, ps):
     w = random_workload(100 + hq, hq=hq, hkv=hkv, d=d, kv_dtype="f32", page_size=ps, max_seg=300, n_req=24)
     for kw in (dict(), dict(force_class=1, min_sep_len=0), dict(rows_min=8, min_sep_len=0)):
         _check_sim(w, **kw)
+
+
+def test_dense_grid_cap():
+    """The planner caps the dense grid only when the dense pass alone would fill the GPU
+    and both passes are large (C4, C5 shapes); a small dense pass (C2) or a
+    streaming-dominated batch (C3) keeps one CTA per SM."""
+    import ctypes as C
+    L = B.lib()
+    f = L.blend_internal_dense_ctas
+    f.restype, f.argtypes = C.c_int32, [C.c_void_p]
+    caps = {n: f(build_tree(W.by_name(n), num_sms=148).handle) for n in ("c2", "c3", "c4", "c5")}
+    assert caps["c2"] == 0 and caps["c3"] == 0
+    for n in ("c4", "c5"):
+        assert int(0.4 * 148) <= caps[n] < 148, caps
