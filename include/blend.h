@@ -199,12 +199,12 @@ typedef struct {
   void* out;                 /* device [sum q, Hq, D] (kv dtype), written                    */
   float* lse;                /* device [sum q, Hq] fp32 natural-log LSE, written             */
   void* workspace;           /* device, >= blend_workspace_bytes (always required): partial
-                                (o, lse) rows, the streaming pass's unit counter and the
-                                arrival counters [merge list][Hq] with which the last
-                                producer of a (token, head) merges it (no merge launch).
-                                ZERO-FILL IT ONCE after allocation; every completed call
-                                leaves the counters at zero again.  One call in flight per
-                                workspace                                                   */
+                                (o, lse) rows, the streaming pass's unit counter (reset by
+                                every call) and the arrival counters [partial row][Hq] of
+                                BLEND_ARRIVAL_MERGE.  With that flag, ZERO-FILL the
+                                workspace once after allocation (every completed call leaves
+                                the counters at zero again); otherwise its contents are
+                                scratch.  One call in flight per workspace                  */
   size_t workspace_bytes;
   const blend_plan* plan;    /* from blend_plan_upload (its buffer must be resident)         */
   int32_t path;              /* BLEND_PATH_*: AUTO = tcgen05 dense + streaming (+ generic for
