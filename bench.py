@@ -253,14 +253,25 @@ def run_ours(args):
     tree_kw = dict(num_sms=torch.cuda.get_device_properties(local).multi_processor_count,
                    dense_split=args.dense_split, split_tokens=args.split_tokens)
 
-    gw = make_workload(args.workload, world)
     t0 = time.perf_counter()
-    if world > 1:
-        gtree = build_tree(gw, **tree_kw)
-        req_shard, _ = gtree.shard(world)
-        w = subset(gw, np.nonzero(req_shard == rank)[0], name=f"{gw.name}_shard{rank}")
+    if args.tp:
+        # NEXT-4: head-parallel replicas — every rank runs the whole
+        # batch for its Hkv/N kv heads and their query-head groups (no exchange inside
+        # attention); strong scaling of one batch.  Synthetic values use local head indices.
+        from dataclasses import replace as _replace
+        gw = make_workload(args.workload, 1)
+        if gw.num_kv_heads % world:
+            raise SystemExit(f"--tp: {gw.num_kv_heads} kv heads do not split over {world} ranks")
+        w = _replace(gw, num_q_heads=gw.num_q_heads // world, num_kv_heads=gw.num_kv_heads // world,
+                     name=f"{gw.name}_tp{world}_rank{rank}")
     else:
-        w = gw
+        gw = make_workload(args.workload, world)
+        if world > 1:
+            gtree = build_tree(gw, **tree_kw)
+            req_shard, _ = gtree.shard(world)
+            w = subset(gw, np.nonzero(req_shard == rank)[0], name=f"{gw.name}_shard{rank}")
+        else:
+            w = gw
     db = device_batch(w, tree_kw=tree_kw)
     host_s = time.perf_counter() - t0
     view = db.view
@@ -318,7 +329,8 @@ def run_ours(args):
     tok = torch.tensor([float(w.sum_q)], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(loc, op=dist.ReduceOp.MAX)
-        dist.all_reduce(tok, op=dist.ReduceOp.SUM)
+        if not args.tp:   # TP: every rank works on the same tokens (its share of the heads)
+            dist.all_reduce(tok, op=dist.ReduceOp.SUM)
     ms, md, mst, mm, mser = loc.tolist()
     total_tok = tok.item()
     value = total_tok / (ms * 1e-3)
@@ -428,11 +440,15 @@ def run_ours(args):
                        "kind": "oracle", "sample": f"failed: {e}"}
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if args.tp else "weak",
             "vs_baseline": None, "dtype": "bf16" if w.kv_dtype == "bf16" else "f32", "data": "synthetic",
             "config": {"workload": gw.name, "requests": gw.n_req, "query_tokens": int(total_tok),
-                       "heads": f"{w.num_q_heads}/{w.num_kv_heads}x{w.head_dim}", "page_size": w.page_size,
-                       "parallelism": f"dp{world} (subtree shards)" if world > 1 else "single GPU",
+                       "heads": f"{gw.num_q_heads}/{gw.num_kv_heads}x{gw.head_dim}"
+                                + (f" (per rank {w.num_q_heads}/{w.num_kv_heads})" if args.tp else ""),
+                       "page_size": w.page_size,
+                       "parallelism": (f"tp{world} (kv heads)" if args.tp else f"dp{world} (subtree shards)")
+                       if world > 1 else ("tp1 (kv heads)" if args.tp else "single GPU"),
                        "l2": "flushed (256 MB write) between timed steps" if do_flush else "not flushed",
                        "path": args.path},
             "clocks": clk,
@@ -474,6 +490,8 @@ def main():
     ap.add_argument("--dense-split", type=int, default=0, help="dense split-KV factor (0 = planner auto)")
     ap.add_argument("--split-tokens", type=int, default=0, help="streaming split-KV chunk (0 = auto)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tp", action="store_true",
+                    help="head-parallel replicas (NEXT-4): each rank takes Hkv/N kv heads of the whole batch")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

@@ -298,3 +298,17 @@ def test_sharded_equals_single_gpu(G):
             seen[r] = True
         _cmp(ws, db, requests=list(range(0, ws.n_req, max(1, ws.n_req // 6))))
     assert seen.all(), "every request in exactly one shard"
+
+
+def test_tp_head_slice():
+    """NEXT-4 head-parallel replicas: a rank's slice of the heads (Hq/N query heads over
+    Hkv/N kv heads, whole batch) is an ordinary plan; C5-shaped groups (g = 8) sliced to
+    one kv head match the oracle."""
+    from dataclasses import replace
+    w0 = W.c2_mmlu_decode(n_req=40)
+    for hq, hkv in ((8, 2), (4, 1)):
+        w = replace(w0, num_q_heads=hq, num_kv_heads=hkv, name=f"{w0.name}_tp_{hq}_{hkv}")
+        db = device_batch(w)
+        db.run()
+        torch.cuda.synchronize()
+        _cmp(w, db)
