@@ -260,10 +260,11 @@ def run_ours(args):
         # attention); strong scaling of one batch.  Synthetic values use local head indices.
         from dataclasses import replace as _replace
         gw = make_workload(args.workload, 1)
-        if gw.num_kv_heads % world:
-            raise SystemExit(f"--tp: {gw.num_kv_heads} kv heads do not split over {world} ranks")
-        w = _replace(gw, num_q_heads=gw.num_q_heads // world, num_kv_heads=gw.num_kv_heads // world,
-                     name=f"{gw.name}_tp{world}_rank{rank}")
+        tpn = args.tp_ranks if args.tp_ranks else world   # --tp-ranks: one rank's slice of a wider TP group
+        if gw.num_kv_heads % tpn:
+            raise SystemExit(f"--tp: {gw.num_kv_heads} kv heads do not split over {tpn} ranks")
+        w = _replace(gw, num_q_heads=gw.num_q_heads // tpn, num_kv_heads=gw.num_kv_heads // tpn,
+                     name=f"{gw.name}_tp{tpn}_rank{rank}")
     else:
         gw = make_workload(args.workload, world)
         if world > 1:
@@ -448,7 +449,8 @@ def run_ours(args):
                                 + (f" (per rank {w.num_q_heads}/{w.num_kv_heads})" if args.tp else ""),
                        "page_size": w.page_size,
                        "parallelism": (f"tp{world} (kv heads)" if args.tp else f"dp{world} (subtree shards)")
-                       if world > 1 else ("tp1 (kv heads)" if args.tp else "single GPU"),
+                       if world > 1 else ((f"one rank of tp{args.tp_ranks} (kv heads)" if args.tp_ranks
+                                           else "tp1 (kv heads)") if args.tp else "single GPU"),
                        "l2": "flushed (256 MB write) between timed steps" if do_flush else "not flushed",
                        "path": args.path},
             "clocks": clk,
@@ -492,6 +494,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--tp", action="store_true",
                     help="head-parallel replicas (NEXT-4): each rank takes Hkv/N kv heads of the whole batch")
+    ap.add_argument("--tp-ranks", type=int, default=0,
+                    help="with --tp on one GPU: time one rank's slice of a TP group of this size "
+                         "(the line's value is that rank's tokens/s, not a group total)")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
