@@ -39,6 +39,9 @@ namespace blend {
 #define DN_NSTAGE128 4     // K/V ring stages at D = 128 (64 keys each)
 #define DN_STAGED_EPI 1    // epilogue through the smem staging tile (else per-thread row stores)
 #endif
+#ifndef BLEND_TRACE_WARPS
+#define BLEND_TRACE_WARPS 0    // 1: per-warp P hand-off stamps for blocks 20..23 of the first unit
+#endif
 #ifndef BLEND_TRACE_UNITS
 #define BLEND_TRACE_UNITS 0    // 1: per-unit start / epilogue-end stamps (first 10 units of each CTA)
 #endif
@@ -528,6 +531,9 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&p_full[t * 2 + buf]);
+#if BLEND_TRACE_WARPS
+        if (lane == 0 && ui == (int)blockIdx.x && j >= 20 && j < 24) trace_stamp(p, 24 + (j - 20) * 8 + (warp - 4));
+#endif
 #if BLEND_TRACE_BLOCKS
         if (threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 9 + 2 * j);
 #endif
