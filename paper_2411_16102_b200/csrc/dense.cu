@@ -4,26 +4,32 @@
 // once by all the SMALL requests under it (PAPER §5 P:11 "exactly-once computation
 // of shared prefixes"; §7.2 P:248-251 cascade reuse of the shared KV access), or a
 // BIG request (chunked prefill) — are dense contractions: up to 256 query
-// rows (tokens x grouped q heads) against 128-key blocks of the node's pages.
+// rows (tokens x grouped q heads) against 64-key blocks of the node's pages.
 //
 // One persistent CTA per SM, warp-specialised, two 128-row Q tiles (A, B) that
 // share every K/V block ("ping-pong": the tensor pipe works on one tile while the
 // other tile's softmax runs):
-//   warp 0       TMA producer: K/V page entries (128B swizzle) -> smem stage ring
-//   warp 1       MMA issuer (one thread): S_t = Q_t K^T (UMMA 128x128x16, K-major
-//                A/B from smem) into TMEM; O_t += P_t V with P_t read from TMEM
-//                (aliasing S_t) and V MN-major from smem; tcgen05.commit -> mbarriers
-//   warp 2       TMEM allocator (512 columns: S_A | S_B | O_A | O_B)
-//   warp 3       Q loader: gathers the next unit's 256 query rows (cp.async, 128B
-//                swizzle) as soon as the current unit's last QK has been issued
+//   warp 0       TMA producer: 64-key K/V blocks (page entries, 128B swizzle) into a
+//                4-stage smem ring
+//   warp 1       MMA issuer (whole warp, one elected lane issues): S_t = Q_t K^T (UMMA
+//                128x64x16, K-major A/B) into one of two TMEM S buffers per tile;
+//                O_t += P_t V with P_t read from TMEM (aliasing its S buffer) and V
+//                MN-major from smem; tcgen05.commit -> mbarriers
+//   warp 2       TMEM allocator (512 columns: S_A0 S_A1 | S_B0 S_B1 | O_A | O_B)
+//   warp 3       Q loader: the next unit's Q tiles as soon as the current unit's last
+//                QK has been issued — 3-D TMA boxes {64, g, 128/g} when the unit's
+//                tokens are consecutive rows of q, one box per token otherwise,
+//                cp.async row gathers when g does not divide 128
 //   warps 4..7   softmax / epilogue of tile A, warps 8..11 of tile B: thread =
 //                query row = TMEM lane; tcgen05.ld the S row, per-row causal mask,
 //                log2-domain online softmax with lazy O rescaling (only when the
-//                running max grows by > 8), P -> bf16 -> tcgen05.st into TMEM,
-//                final O / l -> bf16 row or fp32 partial.
-// MMAs of one thread execute in issue order, so QK_t(j+1) (which overwrites S_t
-// and hence P_t) is issued right after PV_t(j) without a further barrier, and the
-// commit after QK_t(j+1) also certifies PV_t(j) (the softmax may then rescale O_t).
+//                running max grows by > 2^8; blocks whose exponentials sum to <= 2^8
+//                against the running reference skip the block max), exp2 3/4 on
+//                MUFU and 1/4 as an FMA-pipe polynomial, P -> bf16 -> tcgen05.st,
+//                final O / l through a per-warp smem staging tile with coalesced
+//                row-segment stores (bf16 output rows or fp32 partial rows).
+// MMAs of one thread execute in issue order, so QK_t(j+2) (which overwrites the S
+// buffer holding P_t(j)) is issued right after PV_t(j) without a further barrier.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <math.h>
