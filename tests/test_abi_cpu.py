@@ -202,3 +202,16 @@ def test_dense_grid_cap():
     assert caps["c2"] == 0 and caps["c3"] == 0
     for n in ("c4", "c5"):
         assert int(0.4 * 148) <= caps[n] < 148, caps
+
+
+def test_plan_simulation_stream_tail_split():
+    """Streaming tail balance: with 40 decodes x 8 kv heads = 320 streaming units on
+    4 x 13 = 52 rings the last round would be 8 units, so the planner splits the
+    shortest items in two; the plan still reproduces the oracle and every split token
+    gets one more source."""
+    w = W.c2_mmlu_decode(n_req=40)
+    t0 = build_tree(w, num_sms=16)           # 320 % 64 == 0: no split
+    t1 = _check_sim(w, num_sms=13)           # 320 % 52 == 8: split
+    i0, i1 = t0.plan_info(), t1.plan_info()
+    assert i1["n_stream_units"] > i0["n_stream_units"]
+    assert i1["n_partial_rows"] > i0["n_partial_rows"]
