@@ -81,6 +81,15 @@ __host__ __device__ inline DenseSmem dense_layout(int D) {
   return L;
 }
 
+// The k-th unit of this CTA: units are sorted longest first and dealt out in a snake
+// (round k even: CTA b takes k*G + b, odd: k*G + G-1-b), which balances the CTAs' totals
+// far better than plain round robin (the longest of every round no longer lands on the
+// same CTA).  Every warp of the CTA walks the same sequence.
+__device__ __forceinline__ int snake_unit(int k) {
+  const int G = (int)gridDim.x, b = (int)blockIdx.x;
+  return k * G + ((k & 1) ? (G - 1 - b) : b);
+}
+
 // POLY: bit k set -> pair k (of 16 per 32-key chunk) takes the FMA-pipe polynomial exp2
 template <int D, int BOX, uint32_t POLY = 0x8888u>
 __global__ void __launch_bounds__(DN_THREADS, 1)
@@ -151,7 +160,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       ptx::tma_prefetch_desc(&tmv);
       const int4* ents = reinterpret_cast<const int4*>(p.entries);
       uint32_t kit = 0;
-      int ui = blockIdx.x;
+      int uk = 0, ui = snake_unit(0);
       Unit u = ui < p.n_units ? p.units[ui] : Unit{};
       int4 cur[EPB];
       auto load_block = [&](const Unit& un, int j) {
@@ -167,7 +176,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       if (ui < p.n_units) load_block(u, 0);
       while (ui < p.n_units) {
         const int nb = (u.entry_end - u.entry_begin + EPB - 1) / EPB;
-        const int ui_next = ui + gridDim.x;
+        const int ui_next = snake_unit(++uk);
         const Unit un = ui_next < p.n_units ? p.units[ui_next] : Unit{};
         for (int j = 0; j < nb; ++j, ++kit) {
           const uint32_t s = kit % NS, ph = (kit / NS) & 1;
@@ -202,7 +211,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       ptx::tma_prefetch_desc(&tmq1);
     }
     uint32_t gu = 0;
-    for (int ui = blockIdx.x; ui < p.n_units; ui += gridDim.x, ++gu) {
+    for (int uk = 0, ui = snake_unit(0); ui < p.n_units; ui = snake_unit(++uk), ++gu) {
       const Unit u = p.units[ui];
       const int qt0 = p.dqtok[ui];
       if (gu > 0) ptx::mbar_wait(q_empty, (gu - 1) & 1);
@@ -291,7 +300,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       const uint32_t leader = ptx::elect_one();
       uint32_t kit = 0, gu = 0;
       uint32_t pbits = 0;               // parity of the next p_full[tile][buffer] completion (bit pi)
-      for (int ui = blockIdx.x; ui < p.n_units; ui += gridDim.x) {
+      for (int uk = 0, ui = snake_unit(0); ui < p.n_units; ui = snake_unit(++uk)) {
         const Unit u = p.units[ui];
         const int nb = (u.entry_end - u.entry_begin + EPB - 1) / EPB;
         const int ntile = u.n_rows > 128 ? 2 : 1;
@@ -384,13 +393,12 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         enext[i] = v;
       }
     };
-    for (int ui = blockIdx.x; ui < p.n_units; ui += gridDim.x) {
+    for (int uk = 0, ui = snake_unit(0); ui < p.n_units; ui = snake_unit(++uk)) {
       const Unit u = p.units[ui];
       const int nb = (u.entry_end - u.entry_begin + EPB - 1) / EPB;
       if (t == 1 && u.n_rows <= 128) continue;       // tile B idle for this unit
       const int row = 128 * t + r;                    // row within the unit
 #if BLEND_TRACE_UNITS
-      const int uk = (ui - (int)blockIdx.x) / (int)gridDim.x;   // this CTA's k-th unit
       if (threadIdx.x == 128 && uk < 10) trace_stamp(p, 20 + 2 * uk);
 #endif
       int32_t pos = INT32_MIN, token = 0, head = 0, tgt = PM_SKIP;
