@@ -312,3 +312,17 @@ def test_tp_head_slice():
         db.run()
         torch.cuda.synchronize()
         _cmp(w, db)
+
+
+@pytest.mark.parametrize("seed", range(8, 16))
+def test_random_trees_bf16_long(seed):
+    """Longer nodes (up to 400 tokens per segment): multi-block dense
+    units, split-KV streaming, partial tiles and causal diagonals at scale."""
+    hq, hkv = [(8, 1), (8, 2), (32, 8), (16, 4)][seed % 4]
+    w = random_workload(seed, hq=hq, hkv=hkv, d=128 if seed % 3 else 64, kv_dtype="bf16",
+                        page_size=[64, 16, 32, 128][seed % 4], max_seg=400, n_req=int(12 + seed))
+    for kw in (dict(), dict(force_class=1, min_sep_len=0), dict(split_tokens=128)):
+        db = device_batch(w, tree_kw=kw)
+        db.run()
+        torch.cuda.synchronize()
+        _cmp(w, db)
