@@ -326,3 +326,16 @@ def test_random_trees_bf16_long(seed):
         db.run()
         torch.cuda.synchronize()
         _cmp(w, db)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_random_trees_fp32(seed):
+    """fp32 debug path (generic FMA executor + merge kernel) on random forests, 1e-5."""
+    hq, hkv = [(2, 1), (4, 2), (8, 1), (4, 4)][seed]
+    w = random_workload(200 + seed, hq=hq, hkv=hkv, d=64 if seed % 2 else 128, kv_dtype="f32",
+                        page_size=[16, 32, 64, 128][seed], max_seg=120, n_req=10 + 3 * seed)
+    for kw in (dict(), dict(force_class=1, min_sep_len=0), dict(split_tokens=32)):
+        db = device_batch(w, tree_kw=kw)
+        db.run()
+        torch.cuda.synchronize()
+        _cmp(w, db)
