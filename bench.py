@@ -342,31 +342,42 @@ def run_ours(args):
     # (events order each buffer set: H2D -> attention -> D2H -> next H2D into the set).
     q_host = torch.empty(db.q.shape, dtype=db.q.dtype, pin_memory=True)
     q_host.copy_(db.q)
-    out_host = [torch.empty(db.out.shape, dtype=db.out.dtype, pin_memory=True) for _ in range(2)]
-    lse_host = [torch.empty(db.lse.shape, dtype=db.lse.dtype, pin_memory=True) for _ in range(2)]
-    qd = [db.q, torch.empty_like(db.q)]
-    od = [db.out, torch.empty_like(db.out)]
-    ld = [db.lse, torch.empty_like(db.lse)]
+    io_bytes = 2 * db.q.numel() * db.q.element_size()
+    NB = 4 if io_bytes < (256 << 20) else 2   # buffer sets in flight
+    out_host = [torch.empty(db.out.shape, dtype=db.out.dtype, pin_memory=True) for _ in range(NB)]
+    lse_host = [torch.empty(db.lse.shape, dtype=db.lse.dtype, pin_memory=True) for _ in range(NB)]
+    qd = [db.q] + [torch.empty_like(db.q) for _ in range(NB - 1)]
+    od = [db.out] + [torch.empty_like(db.out) for _ in range(NB - 1)]
+    ld = [db.lse] + [torch.empty_like(db.lse) for _ in range(NB - 1)]
+    # L2: a flush kernel on the compute stream would sit inside this timed region, so the
+    # e2e steps instead use inputs larger than L2 — KV caches under 256 MB are rotated
+    # over 3 copies (each step's cache was last touched two steps earlier, with >= 2x its
+    # size of other traffic in between)
+    kv_bytes = 2 * db.k_cache.numel() * db.k_cache.element_size()
+    nrot = 3 if kv_bytes < (256 << 20) else 1
+    kc = [db.k_cache] + [db.k_cache.clone() for _ in range(nrot - 1)]
+    vc = [db.v_cache] + [db.v_cache.clone() for _ in range(nrot - 1)]
     s_h2d, s_d2h = torch.cuda.Stream(), torch.cuda.Stream()
-    ev_h2d = [torch.cuda.Event() for _ in range(2)]
-    ev_cmp = [torch.cuda.Event() for _ in range(2)]
-    ev_d2h = [torch.cuda.Event() for _ in range(2)]
+    ev_h2d = [torch.cuda.Event() for _ in range(NB)]
+    ev_cmp = [torch.cuda.Event() for _ in range(NB)]
+    ev_d2h = [torch.cuda.Event() for _ in range(NB)]
     e2e_t0, e2e_t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
+    # head start: the device sleeps (outside the timed region) while the host enqueues the
+    # K steps, so the events time the device pipeline, not the Python loop that feeds it
+    torch.cuda._sleep(int(2.0e9 * max(2e-3, K * 150e-6)))
     e2e_t0.record(stream)
     s_h2d.wait_event(e2e_t0)
     s_d2h.wait_event(e2e_t0)
     for k in range(K):
-        b = k & 1
+        b = k % NB
         with torch.cuda.stream(s_h2d):
-            if k >= 2:
+            if k >= NB:
                 s_h2d.wait_event(ev_d2h[b])            # set b's previous result has left the device
             qd[b].copy_(q_host, non_blocking=True)
             ev_h2d[b].record(s_h2d)
         stream.wait_event(ev_h2d[b])
-        if do_flush:
-            B.l2_flush(flush)
-        B.attention(qd[b], db.k_cache, db.v_cache, db.plan, od[b], ld[b], db.ws,
+        B.attention(qd[b], kc[k % nrot], vc[k % nrot], db.plan, od[b], ld[b], db.ws,
                     n_cache_pages=db.n_cache_pages, path=path, stream=stream)
         ev_cmp[b].record(stream)
         with torch.cuda.stream(s_d2h):
@@ -374,9 +385,8 @@ def run_ours(args):
             out_host[b].copy_(od[b], non_blocking=True)
             lse_host[b].copy_(ld[b], non_blocking=True)
             ev_d2h[b].record(s_d2h)
-    stream.wait_event(ev_d2h[(K - 1) & 1])
-    if K >= 2:
-        stream.wait_event(ev_d2h[K & 1])
+    for b in range(min(K, NB)):
+        stream.wait_event(ev_d2h[b])
     e2e_t1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = torch.tensor([e2e_t0.elapsed_time(e2e_t1) / K], dtype=torch.float64, device="cuda")
@@ -386,7 +396,7 @@ def run_ours(args):
     h2d = db.q.numel() * db.q.element_size()
     d2h = db.out.numel() * db.out.element_size() + db.lse.numel() * db.lse.element_size()
     # the copied-back result of the last step equals the device result of the same input
-    e2e_match = bool(torch.equal(out_host[(K - 1) & 1], od[0].cpu()))
+    e2e_match = bool(torch.equal(out_host[(K - 1) % NB], od[0].cpu()))
 
     # ---- output gather over NVLink (timed separately, not in the metric)
     gather_ms = None
@@ -457,8 +467,10 @@ def run_ours(args):
             "e2e": {"value": total_tok / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
                     "note": "blend_attention with Q copied in from pinned host memory and out + lse copied "
-                            "back every step; copies on side streams, double-buffered (step k's D2H "
-                            "overlaps step k+1's attention)", "output_matches_device": e2e_match},
+                            "back every step; copies on side streams, NB buffer sets (step k's D2H "
+                            "overlaps step k+1's attention and step k+2's upload)", "buffer_sets": NB, "output_matches_device": e2e_match,
+                    "l2": (f"KV rotated over {nrot} copies ({nrot * kv_bytes >> 20} MB > L2), no flush in the "
+                           "timed region" if nrot > 1 else "inputs larger than L2, no flush in the timed region")},
             "gpu_launches": launches_per_step * K,
             "roofline": roof,
             "cpu_baseline": cpu,
