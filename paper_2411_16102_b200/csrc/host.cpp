@@ -543,8 +543,9 @@ int build_plan(blend_tree* t) {
   // dense split-KV: the dense grid overlaps the streaming grid (PDL), so give it the
   // share of the SMs proportional to its estimated time (NEXT-1, the paper's resource
   // overlap f = max, §2.4) and split its items until that share is filled.
-  // Rates are planning constants measured on B200 for the two kernels (~250 TFLOP/s for
-  // the short dense units this split targets, ~6 TB/s streaming).
+  // Rates are planning constants measured on B200 for the two kernels (~800 TFLOP/s
+  // dense, ~6 TB/s streaming; a 250 TFLOP/s estimate gave the dense pass twice the SMs
+  // the streaming pass could spare: C2 47.3 us with 64 dense CTAs, 43.7 us with 32).
   // When the dense pass alone would fill the GPU and both passes are substantial, cap
   // its grid so the overlapped streaming grid starts on the remaining SMs at once
   // (measured on B200: C4 -2 %, C5 -3 % with caps near these shares; the share moves
@@ -559,7 +560,7 @@ int build_plan(blend_tree* t) {
   int64_t dsplit = 1;
   if (a.dense_split > 0) dsplit = a.dense_split;
   else if (base_d > 0 && base_d < num_sms) {
-    const double t_d = flops_d / 250e12, t_s = bytes_s / 6e12;
+    const double t_d = flops_d / 800e12, t_s = bytes_s / 6e12;
     const double share = t_d / (t_d + t_s);
     const int64_t dense_sms = std::max<int64_t>(1, (int64_t)(share * num_sms + 0.5));
     dsplit = std::max<int64_t>(1, (dense_sms + base_d / 2) / base_d);
