@@ -14,6 +14,7 @@ extern "C" int blend_internal_tree_dims(const blend_tree* t, int32_t* dims);
 extern "C" int64_t blend_internal_partial_rows(const blend_tree* t);
 extern "C" int64_t blend_internal_stream_entries(const blend_tree* t);
 extern "C" int64_t blend_internal_merge_unfused(const blend_tree* t);
+extern "C" int32_t blend_internal_merge_nsrc(const blend_tree* t);
 extern "C" int32_t blend_internal_dense_ctas(const blend_tree* t);
 
 namespace blend {
@@ -64,6 +65,7 @@ extern "C" int blend_plan_upload(const blend_tree* tree, void* dev_buf, size_t b
   plan->count[blend::SEC_COUNT] = blend_internal_partial_rows(tree);
   plan->count[blend::SEC_COUNT + 1] = blend_internal_stream_entries(tree);
   plan->count[blend::SEC_COUNT + 2] = blend_internal_merge_unfused(tree);
+  plan->off[blend::SEC_COUNT] = blend_internal_merge_nsrc(tree);   // (off[] past the sections: plan scalars)
   int32_t dims[5];
   blend_internal_tree_dims(tree, dims);
   plan->num_q_heads = dims[0];
@@ -176,6 +178,7 @@ extern "C" int blend_attention(const blend_attn_args* a, void* stream) {
   AttnParams pm = p;
   pm.n_merge = (int32_t)pl.count[SEC_COUNT + 2];   // fused lists are merged by the streaming pass
   pm.trace = g_trace;
+  pm.merge_nsrc = (int32_t)pl.off[SEC_COUNT];
   if (!arrival) {
     e = launch_merge(pm, st, overlap);
     if (e != cudaSuccess) return cuda_fail(e);

@@ -42,6 +42,7 @@ struct AttnParams {
   const int32_t* dqtok;  // dense units: first token when the unit's tokens are consecutive, else -1
   int32_t n_tokens;      // query tokens (rows of q / out)
   int32_t dense_ctas;    // dense grid cap from the planner (0: one CTA per SM)
+  int32_t merge_nsrc;    // > 0: every unfused merge list has this many sources
   unsigned long long* trace;   // diagnostics only (blend_internal_set_trace): [CTA][64] globaltimer stamps
 };
 
@@ -149,7 +150,10 @@ __device__ __forceinline__ void warp_merge_heads(const AttnParams& p, int m, int
   // together (half the warps of one head per warp, so the grid fits one wave).  32-bit
   // index math, MUFU ex2 / lg2 / rcp, and one vector store per lane and head.
   const int token = p.merge_tok[m];
-  const int s0 = p.merge_off[m], s1 = p.merge_off[m + 1];
+  // every unfused list of the plan has merge_nsrc sources (e.g. one dense + one streaming
+  // partial per decode token): list m is rows m*n .. m*n+n-1, no merge_off round trip
+  const int s0 = p.merge_nsrc > 0 ? m * p.merge_nsrc : p.merge_off[m];
+  const int s1 = p.merge_nsrc > 0 ? s0 + p.merge_nsrc : p.merge_off[m + 1];
   const int D = p.d, hq = p.hq;
   const int vec = D / 32;          // 2 or 4 elements per lane
   const int e0 = lane * vec;

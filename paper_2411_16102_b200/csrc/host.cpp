@@ -103,6 +103,7 @@ struct blend_tree {
   int64_t stream_entries = 0;   // sum over stream units of their entry counts (launch heuristic)
   int32_t n_merge_unfused = 0;  // merge lists [0, n) are merged by the merge kernel
   int32_t dense_ctas = 0;       // dense-pass grid cap (0: one CTA per SM), set by the planner
+  int32_t merge_nsrc = 0;       // > 0: every unfused merge list has this many sources
 };
 
 namespace {
@@ -732,6 +733,13 @@ int build_plan(blend_tree* t) {
       if (pass == 0) ++n_unfused;
     }
   t->n_merge_unfused = n_unfused;
+  t->merge_nsrc = 0;
+  if (n_unfused > 0) {
+    const int32_t n0 = merge_off[1] - merge_off[0];
+    bool uni = true;
+    for (int32_t m = 1; m < n_unfused && uni; ++m) uni = merge_off[m + 1] - merge_off[m] == n0;
+    if (uni) t->merge_nsrc = n0;
+  }
   if (prow > INT32_MAX / 2) return fail(BLEND_EINVAL, "too many partial rows");
 
   // ---- entries and units
@@ -1099,6 +1107,7 @@ int64_t blend_internal_partial_rows(const blend_tree* t) { return t ? t->n_parti
 int64_t blend_internal_stream_entries(const blend_tree* t) { return t ? t->stream_entries : 0; }
 int64_t blend_internal_merge_unfused(const blend_tree* t) { return t ? t->n_merge_unfused : 0; }
 int32_t blend_internal_dense_ctas(const blend_tree* t) { return t ? t->dense_ctas : 0; }
+int32_t blend_internal_merge_nsrc(const blend_tree* t) { return t ? t->merge_nsrc : 0; }
 
 int blend_internal_tree_dims(const blend_tree* t, int32_t* dims) {
   if (!t) return fail(BLEND_EINVAL, "tree is NULL");
