@@ -68,3 +68,35 @@ def from_paths(paths, q=None, p=None, d=None, hq=2, hkv=1, dim=64, page_size=16,
                     q_len=np.asarray(q if q is not None else [1] * R, dtype=np.int32),
                     prompt_len=np.asarray(p if p is not None else n, dtype=np.int32),
                     out_len=np.asarray(d if d is not None else [16] * R, dtype=np.int32))
+
+
+DEGENERATE = ["one_token", "single_prefill", "identical_decode", "identical_mixed_q", "nested",
+              "long_decode"]
+
+
+def degenerate_workload(case):
+    """Edge-case batches (bf16, 8/2 heads, D=128, ps=64) shared by the plan-simulation
+    and GPU parity tests."""
+    rng = np.random.default_rng(77)
+    tok = lambda n: rng.integers(1000, 32000, n).astype(np.int32)       # noqa: E731
+    if case == "one_token":
+        paths, q = [tok(1)], [1]
+    elif case == "single_prefill":                  # causal prefill from position 0, ragged tail
+        paths, q = [tok(700)], [700]
+    elif case == "identical_decode":                # one node holding every request
+        a = tok(500)
+        paths, q = [a] * 20, [1] * 20
+    elif case == "identical_mixed_q":
+        a = tok(300)
+        paths, q = [a] * 3, [300, 150, 1]
+    elif case == "nested":                          # requests ending inside the tree (interior nodes)
+        a, b, c = tok(400), tok(200), tok(300)
+        paths = [a, np.concatenate([a, b]), np.concatenate([a, b, c]), np.concatenate([a, c])]
+        q = [64, 1, 200, 7]
+    elif case == "long_decode":                     # 64K-token context next to shorter siblings
+        a = tok(32768)
+        paths = [np.concatenate([a, tok(32768)])] + [np.concatenate([a, tok(100 + i)]) for i in range(3)]
+        q = [1, 1, 3, 1]
+    n = [len(x) for x in paths]
+    return from_paths(paths, q=q, p=n, d=[8] * len(paths), hq=8, hkv=2, dim=128, page_size=64,
+                      kv_dtype="bf16", seed=11)

@@ -13,7 +13,7 @@ from oracle import attention as A
 from oracle import shard as OS
 from oracle import tree as OT
 from synth import workloads as W
-from tests.helpers import random_workload
+from tests.helpers import DEGENERATE, degenerate_workload, random_workload
 from tests.plan_sim import simulate
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -75,7 +75,7 @@ def test_big_keys_exact():
     assert max(v_o["cu"]) > 2**80 and max(v_o["mu"]) > 2**62
 
 
-@pytest.mark.parametrize("bad", ["q0", "qbig", "empty", "negtok", "heads", "dim", "ps", "nospc", "dup"])
+@pytest.mark.parametrize("bad", ["q0", "qbig", "empty", "noreq", "negtok", "heads", "dim", "ps", "nospc", "dup"])
 def test_rejections_match(bad):
     from tests.helpers import from_paths
     w = from_paths([[1, 2, 3], [1, 2, 4]])
@@ -86,6 +86,8 @@ def test_rejections_match(bad):
         w.q_len[0] = 4
     elif bad == "empty":
         w = from_paths([[1, 2, 3], []])
+    elif bad == "noreq":
+        w = from_paths([])
     elif bad == "negtok":
         w.tokens[1] = -5
     elif bad == "heads":
@@ -215,3 +217,11 @@ def test_plan_simulation_stream_tail_split():
     i0, i1 = t0.plan_info(), t1.plan_info()
     assert i1["n_stream_units"] > i0["n_stream_units"]
     assert i1["n_partial_rows"] > i0["n_partial_rows"]
+
+
+@pytest.mark.parametrize("case", DEGENERATE)
+@pytest.mark.parametrize("kw", [dict(), dict(force_class=1, min_sep_len=0, dense_split=3),
+                                dict(force_class=2, split_tokens=64)])
+def test_plan_simulation_degenerate(case, kw):
+    """The plan of each edge-case batch computes the oracle's attention in fp64."""
+    _check_sim(degenerate_workload(case), **kw)

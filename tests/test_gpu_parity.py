@@ -339,3 +339,19 @@ def test_random_trees_fp32(seed):
         db.run()
         torch.cuda.synchronize()
         _cmp(w, db)
+
+
+@pytest.mark.parametrize("case", ["one_token", "single_prefill", "identical_decode",
+                                  "identical_mixed_q", "nested", "long_decode"])
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("kw", [dict(), dict(force_class=1, min_sep_len=0, dense_split=3),
+                                dict(force_class=2, split_tokens=64)])
+def test_degenerate_shapes(case, path, kw):
+    """Edge cases of the method: a one-token batch, a full causal prefill, identical paths
+    (one node, no private suffix), requests that end at interior nodes, a 64K context."""
+    from tests.helpers import degenerate_workload
+    w = degenerate_workload(case)
+    db = device_batch(w, tree_kw=kw)
+    db.run(path=path)
+    torch.cuda.synchronize()
+    _cmp(w, db)
