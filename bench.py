@@ -54,7 +54,7 @@ def load_peaks():
     return d
 
 
-PROFILE_TAG = "r1g"   # profiles/<tag>_ncu.json: ncu --set full captures of this code's kernels
+PROFILE_TAG = "r1h"   # profiles/<tag>_ncu.json: ncu --set full captures of this code's kernels
 
 
 def ncu_traffic(workload: str, kernel: str):
