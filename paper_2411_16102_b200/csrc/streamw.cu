@@ -33,6 +33,9 @@ namespace blend {
 #define SW_WARPS_CFG 4
 #define SW_STAGES_CFG 3
 #endif
+#ifndef SW_Q_AFTER
+#define SW_Q_AFTER 1   // the next unit's Q rows are requested after this many stages of the current one
+#endif
 constexpr int SW_WARPS = SW_WARPS_CFG;                  // consumer warps = rings = producer warps
 constexpr int SW_THREADS = 32 * (2 * SW_WARPS);
 constexpr int SW_STAGES = SW_STAGES_CFG;
@@ -294,6 +297,7 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
     __syncwarp();   // every lane's ldmatrix of this buffer is done before the next prefetch targets it later
     nann = next_index();
     bool q_pending = nann.x < p.n_units;
+    int q_wait = 0;   // stages of this unit done (the next unit's Q is issued after SW_Q_AFTER)
     if (q_pending) pre = prefetch(nann);
     const int32_t pos0r = cu.d0.qrow >= 0 ? cu.d0.pos : INT32_MIN;
     const int32_t pos1r = cu.d1.qrow >= 0 ? cu.d1.pos : INT32_MIN;
@@ -408,7 +412,7 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
 #if BLEND_TRACE_STAGES
         if (warp == 0 && lane == 0 && it >= 4 && it < 12) trace_stamp_s(p, 44 + (it - 4));
 #endif
-        if (q_pending) {
+        if (q_pending && ++q_wait >= SW_Q_AFTER) {
           issue_q(pre, buf ^ 1);
           q_pending = false;
         }
