@@ -53,20 +53,11 @@ def weights(w, view, kappa: int):
     return sigma, wt
 
 
-def shard_assign(w, view, n_shards: int, kappa: int = 213):
-    """req_shard[R] (int32) for G = n_shards."""
-    G = n_shards
-    if G < 1:
-        raise T.BlendError(T.EINVAL, "n_shards must be >= 1")
-    sigma, wt = weights(w, view, kappa)
-    R = len(sigma)
-    S = [0]
-    for r in sigma:
-        S.append(S[-1] + wt[r])
+def cut_points(S, lcp, G):
+    """Steps 3-4: block boundaries k_0 = 0 <= k_1 <= ... <= k_{2G-1} <= k_{2G} = R over
+    the prefix sums S[0..R] (S[0] = 0) and the lcp[k] of the pair (sigma_{k-1}, sigma_k)."""
+    R = len(S) - 1
     W = S[-1]
-    lcp = [0] * (R + 1)
-    for k in range(1, R):
-        lcp[k] = _lcp(w.path(sigma[k - 1]), w.path(sigma[k]))
     cuts = [0]
     for i in range(1, 2 * G):
         tau = -(-(i * W) // (2 * G))
@@ -77,6 +68,23 @@ def shard_assign(w, view, n_shards: int, kappa: int = 213):
             k = min(range(R + 1), key=lambda k: (abs(S[k] - tau), k))
         cuts.append(max(k, cuts[-1]))
     cuts.append(R)
+    return cuts
+
+
+def shard_assign(w, view, n_shards: int, kappa: int = 213):
+    """req_shard[R] (int32) for G = n_shards."""
+    G = n_shards
+    if G < 1:
+        raise T.BlendError(T.EINVAL, "n_shards must be >= 1")
+    sigma, wt = weights(w, view, kappa)
+    R = len(sigma)
+    S = [0]
+    for r in sigma:
+        S.append(S[-1] + wt[r])
+    lcp = [0] * (R + 1)
+    for k in range(1, R):
+        lcp[k] = _lcp(w.path(sigma[k - 1]), w.path(sigma[k]))
+    cuts = cut_points(S, lcp, G)
     req_shard = np.zeros(w.n_req, dtype=np.int32)
     for j in range(2 * G):
         g = j if j < G else 2 * G - 1 - j

@@ -82,3 +82,31 @@ def test_shard_trees_restrict():
     for s in subs:
         assert list(s.global_id) == sorted(s.global_id)
         T.build(s)
+
+
+def test_cut_targets_round_up():
+    # §8(c-3) step 3: tau_i = ceil(i W / 2G).  G = 1, W = 7: tau = 4, and the only prefix
+    # sum within the window |S_k - tau| * 32 <= 7 is S_2 = 4 (a round-down target 3 would
+    # have no candidate and tie S_1 = 2 / S_2 = 4, taking k = 1).
+    assert S.cut_points([0, 2, 4, 7], [0, 0, 0, 0], 1) == [0, 2, 3]
+    # G = 2, W = 10: tau = 3, 5, 8 (ceil of 2.5, 5, 7.5)
+    assert S.cut_points([0, 3, 5, 7, 8, 10], [0] * 6, 2) == [0, 1, 2, 4, 5]
+
+
+def test_cut_prefers_subtree_boundary_in_window():
+    # step 4: inside the window the smallest lcp wins over the closest prefix sum
+    Ssum = [0] + list(range(10, 330, 10))                  # W = 320, G = 1: tau = 160, window +-10
+    lcp = [0] + [5] * 31 + [0]
+    lcp[17] = 1                                          # S_17 = 170 is 10 from tau
+    assert S.cut_points(Ssum, lcp, 1) == [0, 17, 32]
+    lcp[15] = 1                                          # S_15 = 150, also 10 from tau
+    assert S.cut_points(Ssum, lcp, 1) == [0, 15, 32]       # |150-160| = |170-160|: smaller k
+    lcp[16] = 1
+    assert S.cut_points(Ssum, lcp, 1) == [0, 16, 32]       # exact hit at equal lcp
+
+
+def test_cuts_fallback_heavy_request():
+    # step 4 fallback (no prefix sum in the window): nearest prefix sum, ties to the smaller
+    # k.  One heavy request (weight 99 of W = 101) spans targets tau = 13, 26, 38, 51, 64,
+    # 76, 89 (G = 4); |1 - 51| = 50 > |100 - 51| = 49 moves the cut past it at i = 4.
+    assert S.cut_points([0, 1, 100, 101], [0, 0, 0, 0], 4) == [0, 1, 1, 1, 2, 2, 2, 2, 3]

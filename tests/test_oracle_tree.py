@@ -298,3 +298,95 @@ def test_rejections(bad, status):
     with pytest.raises(T.BlendError) as e:
         T.build(w, **kw)
     assert e.value.status == status
+
+
+# ---------------------------------------------------------------------------
+# Density key terms for requests whose cached path length n_r differs from the
+# prompt length p_r (decode state n_r > p_r, chunked-prefill state n_r < p_r).
+# Comp(r) counts (p + d) GEMM tokens and p^2 attention work of the WHOLE
+# request, whatever step of its lifetime the snapshot catches; a set's
+# GEMM tokens are (1 - s) T_comp, i.e. shared prompt tokens count once.
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("p,d,n", [(64, 16, 1), (64, 16, 40), (64, 16, 64), (64, 16, 70), (64, 16, 80),
+                                   (728, 256, 512), (728, 256, 900), (228, 16384, 5000), (1100, 2, 1101)])
+def test_single_request_key_independent_of_lifetime_state(p, d, n):
+    # n < p: prefill state (p - n prompt tokens not yet in the cache); n > p: decode
+    # state (n - p generated tokens cached).  The key is the paper's Comp/Mem of the
+    # request, independent of n.
+    w = from_paths([list(range(1000, 1000 + n))], p=[p], d=[d])
+    v = T.build(w)
+    comp, mem = _comp_mem_single(p, d)
+    assert v["cu"][0] == comp and v["mu"][0] == mem
+
+
+def test_three_level_key_by_hand():
+    # Worked by hand from P:89 (GEMM tokens = prompt + output) and P:315 (shared prompt
+    # tokens counted once).  Tree: N0 (100 tokens, requests A B C) -> N1 (50, A B) ->
+    # leaves a (10, A), b (20, B); N0 -> c (30, C).
+    #   A: path 160 tokens, p = 120 (decode state: prompt = N0 + 20 tokens of N1)
+    #   B: path 170 tokens, p = 200 (prefill state: 30 prompt tokens not yet cached)
+    #   C: path 130 tokens, p = 130
+    # Distinct prompt tokens of {A, B} = N0 100 + N1 50 (B's prompt covers it) + b 20 + B's
+    # 30 uncached = 200; A's leaf holds generated tokens only.  Of {A, B, C}: 200 + c 30.
+    rng = np.random.default_rng(7)
+    n0, n1 = list(rng.integers(1000, 32000, 100)), [50000 + i for i in range(50)]
+    a, b, c = [60000 + i for i in range(10)], [61000 + i for i in range(20)], [62000 + i for i in range(30)]
+    dA, dB, dC = 50, 7, 300
+    w = from_paths([n0 + n1 + a, n0 + n1 + b, n0 + c], p=[120, 200, 130], d=[dA, dB, dC])
+    v = T.build(w)
+    Pm, HL4 = 8_030_261_248, 4 * 4096 * 32
+
+    def node_of(tokens):
+        for i in range(v["n_nodes"]):
+            if _node_tokens(v, w, i) == tuple(tokens):
+                return i
+        raise AssertionError(tokens)
+    mem = lambda p, d: p * d + d * (d + 1) // 2          # noqa: E731  sum_{i=1..d} (p + i)
+    expect = {
+        tuple(n0): (230 + dA + dB + dC, [120, 200, 130], [(120, dA), (200, dB), (130, dC)]),
+        tuple(n1): (200 + dA + dB, [120, 200], [(120, dA), (200, dB)]),
+        tuple(a): (120 + dA, [120], [(120, dA)]),     # single request: G = p + d
+        tuple(b): (200 + dB, [200], [(200, dB)]),
+        tuple(c): (130 + dC, [130], [(130, dC)]),
+    }
+    for toks, (G, ps, pd) in expect.items():
+        i = node_of(toks)
+        assert v["cu"][i] == 2 * Pm * G + HL4 * sum(x * x for x in ps), toks[:2]
+        assert v["mu"][i] == sum(mem(p, d) for p, d in pd)
+
+
+def _bruteforce_key(w, S, Pm, HL4):
+    """G_S = |distinct prompt tokens of S| + sum d_r, a prompt token being identified by
+    its full prefix (tokens up to and including it) when it is cached, and as private
+    (r, j) when it is not yet in the cache (j >= n_r)."""
+    seen = set()
+    for r in S:
+        path = w.path(r)
+        p, n = int(w.prompt_len[r]), len(path)
+        for j in range(min(p, n)):
+            seen.add(tuple(int(x) for x in path[:j + 1]))
+        for j in range(n, p):
+            seen.add(("uncached", r, j))
+    G = len(seen) + sum(int(w.out_len[r]) for r in S)
+    cu = 2 * Pm * G + HL4 * sum(int(w.prompt_len[r]) ** 2 for r in S)
+    mu = sum(int(w.prompt_len[r]) * int(w.out_len[r]) + int(w.out_len[r]) * (int(w.out_len[r]) + 1) // 2
+             for r in S)
+    return cu, mu
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_keys_match_distinct_prompt_bruteforce(seed):
+    # every node's key against the brute-force distinct-prefix count, with prompt lengths
+    # drawn on both sides of the cached path length
+    w = random_workload(seed, max_seg=15, tok_hi=1003 if seed % 4 == 0 else 32000)
+    rng = np.random.default_rng(100 + seed)
+    n = np.diff(w.tok_off)
+    w.prompt_len = np.array([max(0, int(x) + int(rng.integers(-int(x), 12))) for x in n], dtype=np.int32)
+    v = T.build(w)
+    Pm, HL4 = int(w.model_params), 4 * int(w.hidden) * int(w.layers)
+    for i in range(v["n_nodes"]):
+        s, ln = int(v["node_start"][i]), int(v["node_len"][i])
+        full = w.path(int(v["node_first_req"][i]))[:s + ln]
+        S = [r for r in range(w.n_req) if len(w.path(r)) >= s + ln and np.array_equal(w.path(r)[:s + ln], full)]
+        assert len(S) == int(v["node_nreq"][i])
+        assert (v["cu"][i], v["mu"][i]) == _bruteforce_key(w, S, Pm, HL4), i
