@@ -16,14 +16,14 @@ from synth import values as V
 
 
 def build_tree(w, rows_min=128, min_sep_len=128, force_class=0, split_tokens=0, num_sms=148,
-               free_pages=None, dense_split=0, fuse_merge=0):
+               free_pages=None, dense_split=0):
     fp = w.free_pages if free_pages is None else free_pages
     return B.build(w.tokens, w.tok_off, w.q_len, w.prompt_len, w.out_len,
                    num_q_heads=w.num_q_heads, num_kv_heads=w.num_kv_heads, head_dim=w.head_dim,
                    kv_dtype=w.kv_dtype, model_params=w.model_params, hidden=w.hidden, layers=w.layers,
                    page_size=w.page_size, free_pages=fp, global_id=w.global_id, rows_min=rows_min,
                    min_sep_len=min_sep_len, force_class=force_class, split_tokens=split_tokens,
-                   num_sms=num_sms, dense_split=dense_split, fuse_merge=fuse_merge)
+                   num_sms=num_sms, dense_split=dense_split)
 
 
 def page_slot_hashes(w, view):
@@ -98,7 +98,7 @@ def device_batch(w, device="cuda", tree_kw=None, n_cache_pages=None, fill=True) 
     q = torch.zeros((T, w.num_q_heads, w.head_dim), dtype=dt, device=device)
     out = torch.zeros_like(q)
     lse = torch.zeros((T, w.num_q_heads), dtype=torch.float32, device=device)
-    ws = torch.zeros(max(256, tree.workspace_bytes), dtype=torch.uint8, device=device)   # zeroed once (arrival counters)
+    ws = torch.empty(max(256, tree.workspace_bytes), dtype=torch.uint8, device=device)
     plan_buf = torch.empty(max(256, tree.plan_bytes), dtype=torch.uint8, device=device)
     plan = tree.upload_plan(plan_buf)
     if fill:

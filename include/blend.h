@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define BLEND_ABI_VERSION 1
+#define BLEND_ABI_VERSION 2
 
 typedef enum {
   BLEND_OK = 0,
@@ -87,8 +87,6 @@ typedef struct {
   int32_t split_tokens;        /* streaming split-KV chunk in tokens, 0 = auto (plan only)       */
   int32_t num_sms;             /* SM count the plan is sized for, 0 = 148 (B200)                */
   int32_t dense_split;         /* split-KV factor of dense items, 0 = auto (plan only)            */
-  int32_t fuse_merge;          /* 1: a streaming unit whose token's other sources are dense
-                                  partials merges them itself (no merge launch); 0 = off       */
 } blend_build_args;
 
 typedef struct blend_tree blend_tree;   /* opaque, host-owned */
@@ -168,15 +166,21 @@ int blend_plan_get_info(const blend_tree* tree, blend_plan_info* info);
 size_t blend_plan_bytes(const blend_tree* tree);
 size_t blend_workspace_bytes(const blend_tree* tree);
 
-/* Uploaded plan: device pointers into the caller's plan buffer + counts.
- * Fill with blend_plan_upload; treat the fields as opaque. */
+/* Uploaded plan: the caller's plan buffer plus the planner's scalars.  Filled by
+ * blend_plan_upload; read-only for the caller (blend_attention trusts it). */
 typedef struct {
-  const void* dev;           /* caller device buffer holding the plan             */
+  const void* dev;           /* caller device buffer holding the plan                        */
   size_t bytes;
-  int64_t off[16];           /* section offsets inside dev                        */
-  int64_t count[16];         /* section element counts                            */
-  int32_t num_q_heads, num_kv_heads, head_dim, kv_dtype, page_size;
-  int32_t reserved;          /* planner's dense-pass grid cap (0: one CTA per SM)     */
+  int64_t off[16];           /* byte offset of each plan section inside dev (library layout) */
+  int64_t count[16];         /* element count of each plan section                          */
+  int32_t num_q_heads, num_kv_heads, head_dim, kv_dtype, page_size;   /* the tree's build args */
+  int32_t dense_ctas;        /* dense-pass grid cap for the overlapped launch (planner's SM
+                                share for NEXT-1); 0 = one CTA per SM              */
+  int64_t n_partial_rows;    /* partial (o, lse) rows the workspace holds                    */
+  int64_t stream_entries;    /* sum of KV entries over the streaming units (launch sizing)   */
+  int32_t merge_nsrc;        /* > 0: every merge list has exactly this many partial rows     */
+  int32_t max_page;          /* largest physical page id the plan reads (-1: none);
+                                blend_attention requires max_page < n_cache_pages           */
 } blend_plan;
 
 /* Copy the plan (host, inside the tree) into dev_buf (device, >= blend_plan_bytes)
@@ -187,7 +191,7 @@ int blend_plan_upload(const blend_tree* tree, void* dev_buf, size_t bytes, void*
                       blend_plan* plan);
 
 enum { BLEND_PATH_AUTO = 0, BLEND_PATH_GENERIC = 1, BLEND_PATH_NO_TCGEN05 = 2 };
-enum { BLEND_SERIALIZE = 1, BLEND_ARRIVAL_MERGE = 2 };
+enum { BLEND_SERIALIZE = 1 };
 
 typedef struct {
   const void* q;             /* device [sum q, Hq, D] (kv dtype), rows in caller request order:
@@ -199,14 +203,13 @@ typedef struct {
   void* out;                 /* device [sum q, Hq, D] (kv dtype), written                    */
   float* lse;                /* device [sum q, Hq] fp32 natural-log LSE, written             */
   void* workspace;           /* device, >= blend_workspace_bytes (always required): partial
-                                (o, lse) rows, the streaming pass's unit counter (reset by
-                                every call) and the arrival counters [partial row][Hq] of
-                                BLEND_ARRIVAL_MERGE.  With that flag, ZERO-FILL the
-                                workspace once after allocation (every completed call leaves
-                                the counters at zero again); otherwise its contents are
-                                scratch.  One call in flight per workspace                  */
+                                (o, lse) rows and the streaming pass's unit counter (reset by
+                                every call); scratch between calls.  One call in flight per
+                                workspace                                                   */
   size_t workspace_bytes;
   const blend_plan* plan;    /* from blend_plan_upload (its buffer must be resident)         */
+  int32_t dtype;             /* BLEND_BF16 | BLEND_F32: element type of q, k/v caches and out;
+                                must equal the plan's kv_dtype (EINVAL otherwise)           */
   int32_t path;              /* BLEND_PATH_*: AUTO = tcgen05 dense + streaming (+ generic for
                                 fp32); GENERIC = every unit on the fp32-FMA item executor;
                                 NO_TCGEN05 = dense units on the generic executor            */
@@ -215,22 +218,19 @@ typedef struct {
                                 and overlaps the dense pass on free SMs (the two passes are
                                 independent; the streaming grid completes only after the
                                 dense grid) and the merge kernel is a programmatic
-                                dependent of the streaming grid.
-                                BLEND_ARRIVAL_MERGE (bf16, AUTO path): no merge launch; the
-                                last producer of each (token, head) merges it, counted in
-                                on the workspace's arrival counters (measured slower than
-                                the merge launch on decode-heavy batches, hence opt-in)  */
+                                dependent of the streaming grid                            */
   void* events[4];           /* optional cudaEvent_t recorded before dense, before stream,
                                 before merge, after merge (NULL entries skipped); non-NULL
                                 events[1] or events[2] imply BLEND_SERIALIZE                 */
 } blend_attn_args;
 
-/* Enqueue the blended-batch attention on stream.  Every slot of every page the
- * plan references must hold finite values (slots past a node's end included:
- * masked keys get probability 0, and 0 * NaN would poison the output).  Never
- * allocates, never synchronises; asynchronous faults surface at the caller's
- * next synchronisation.  EINVAL (NULLs, dtype mismatch), ENOSPC (workspace),
- * EUNSUPPORTED (not sm_100), ECUDA (launch failure). */
+/* Enqueue the blended-batch attention on stream.  The slots of a node's pages that
+ * hold its tokens must be finite; the slots past a node's end (the tail of its last
+ * page) may hold anything, NaN included: the kernels never let them reach the output.
+ * Never allocates, never synchronises; asynchronous faults surface at the caller's
+ * next synchronisation.  EINVAL (NULLs, dtype != plan kv_dtype, a plan page id
+ * >= n_cache_pages, bad path / flags), ENOSPC (workspace), EUNSUPPORTED (not sm_100),
+ * ECUDA (launch failure). */
 int blend_attention(const blend_attn_args* args, void* stream);
 
 /* ------------------------------------------------------------------------ */

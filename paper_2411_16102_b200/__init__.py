@@ -27,7 +27,6 @@ OK, EINVAL, EMALFORMED, ENOSPC, ECUDA, ENOMEM, EUNSUPPORTED = 0, -1, -2, -3, -4,
 BF16, F32 = 0, 1
 PATH_AUTO, PATH_GENERIC, PATH_NO_TCGEN05 = 0, 1, 2
 SERIALIZE = 1
-ARRIVAL_MERGE = 2
 _DTYPES = {"bf16": BF16, "f32": F32}
 
 
@@ -46,7 +45,7 @@ class BuildArgs(C.Structure):
                 ("layers", C.c_int32), ("page_size", C.c_int32), ("free_pages", C.c_void_p),
                 ("n_free_pages", C.c_int64), ("rows_min", C.c_int32), ("min_sep_len", C.c_int32),
                 ("force_class", C.c_int32), ("split_tokens", C.c_int32), ("num_sms", C.c_int32),
-                ("dense_split", C.c_int32), ("fuse_merge", C.c_int32)]
+                ("dense_split", C.c_int32)]
 
 
 class TreeView(C.Structure):
@@ -67,15 +66,16 @@ class Plan(C.Structure):
     _fields_ = [("dev", C.c_void_p), ("bytes", C.c_size_t), ("off", C.c_int64 * 16),
                 ("count", C.c_int64 * 16), ("num_q_heads", C.c_int32), ("num_kv_heads", C.c_int32),
                 ("head_dim", C.c_int32), ("kv_dtype", C.c_int32), ("page_size", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("dense_ctas", C.c_int32), ("n_partial_rows", C.c_int64), ("stream_entries", C.c_int64),
+                ("merge_nsrc", C.c_int32), ("max_page", C.c_int32)]
 
 
 class AttnArgs(C.Structure):
     _fields_ = [("q", C.c_void_p), ("k_cache", C.c_void_p), ("v_cache", C.c_void_p),
                 ("n_cache_pages", C.c_int64), ("out", C.c_void_p), ("lse", C.c_void_p),
                 ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
-                ("plan", C.POINTER(Plan)), ("path", C.c_int32), ("flags", C.c_int32),
-                ("events", C.c_void_p * 4)]
+                ("plan", C.POINTER(Plan)), ("dtype", C.c_int32), ("path", C.c_int32),
+                ("flags", C.c_int32), ("events", C.c_void_p * 4)]
 
 
 _lib = None
@@ -242,9 +242,17 @@ class Tree:
 def build(tokens, tok_off, q_len, prompt_len, out_len, *, num_q_heads, num_kv_heads, head_dim,
           kv_dtype="bf16", model_params=8_030_261_248, hidden=4096, layers=32, page_size=64,
           free_pages=None, global_id=None, rows_min=128, min_sep_len=128, force_class=0,
-          split_tokens=0, num_sms=148, dense_split=0, fuse_merge=0) -> Tree:
-    """blend_tree_build on host arrays (numpy-convertible)."""
+          split_tokens=0, num_sms=148, dense_split=0) -> Tree:
+    """blend_tree_build on host arrays (numpy-convertible).  Array lengths are checked
+    here (the C side trusts n_req = len(q_len)): ValueError on a mismatch."""
     keep = []
+    R = len(q_len)
+    for name, arr, n in (("tok_off", tok_off, R + 1), ("prompt_len", prompt_len, R), ("out_len", out_len, R)) + \
+            ((("global_id", global_id, R),) if global_id is not None else ()):
+        if len(arr) != n:
+            raise ValueError(f"{name} has {len(arr)} entries, expected {n} (n_req = len(q_len) = {R})")
+    if R and (int(tok_off[0]) != 0 or int(tok_off[-1]) != len(tokens)):
+        raise ValueError(f"tok_off must run from 0 to len(tokens) = {len(tokens)}")
     tok_off, p_off = _arr(tok_off, np.int64); keep.append(tok_off)
     tokens, p_tok = _arr(tokens, np.int32); keep.append(tokens)
     q_len, p_q = _arr(q_len, np.int32); keep.append(q_len)
@@ -263,10 +271,18 @@ def build(tokens, tok_off, q_len, prompt_len, out_len, *, num_q_heads, num_kv_he
         a.n_free_pages = len(fp)
     a.rows_min, a.min_sep_len, a.force_class = rows_min, min_sep_len, force_class
     a.split_tokens, a.num_sms, a.dense_split = split_tokens, num_sms, dense_split
-    a.fuse_merge = fuse_merge
     h = C.c_void_p()
     _check(lib().blend_tree_build(C.byref(a), C.byref(h)))
     return Tree(h.value)
+
+
+def _torch_dtype_code(t) -> int:
+    name = str(t.dtype)
+    if name == "torch.bfloat16":
+        return BF16
+    if name == "torch.float32":
+        return F32
+    return -1                      # rejected by blend_attention (EINVAL)
 
 
 def attention(q, k_cache, v_cache, plan: Plan, out, lse, workspace, *, n_cache_pages: int,
@@ -280,6 +296,7 @@ def attention(q, k_cache, v_cache, plan: Plan, out, lse, workspace, *, n_cache_p
         a.workspace = workspace.data_ptr()
         a.workspace_bytes = workspace.numel() * workspace.element_size()
     a.plan = C.pointer(plan)
+    a.dtype = _torch_dtype_code(q)
     a.path = path
     a.flags = flags
     if events:
@@ -302,6 +319,20 @@ def fill_q(q, dtype, num_q_heads, head_dim, row_gid, row_t, seed, scale_q=1.0, s
                               row_gid.data_ptr(), row_t.data_ptr(), row_gid.numel(),
                               C.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), C.c_float(scale_q),
                               C.c_void_p(_stream_handle(stream))))
+
+
+def set_stats(buf=None):
+    """Diagnostics only: point the calling thread's subsequent blend_attention calls at a
+    device uint64[8] buffer of softmax path counters (csrc/common.cuh STAT_*), or detach
+    (None).  Production calls leave it detached."""
+    L = lib()
+    f = L.blend_internal_set_stats
+    f.restype, f.argtypes = C.c_int, [C.c_void_p]
+    f(None if buf is None else C.c_void_p(buf.data_ptr()))
+
+
+STAT_NAMES = ["dense_blocks", "dense_slow", "dense_slow_late", "dense_rescale", "stream_stages",
+              "stream_rescale", "tail_zeroed"]
 
 
 def l2_flush(buf, stream=None):

@@ -13,25 +13,29 @@ extern "C" int blend_internal_plan_image(const blend_tree* t, const void** data,
 extern "C" int blend_internal_tree_dims(const blend_tree* t, int32_t* dims);
 extern "C" int64_t blend_internal_partial_rows(const blend_tree* t);
 extern "C" int64_t blend_internal_stream_entries(const blend_tree* t);
-extern "C" int64_t blend_internal_merge_unfused(const blend_tree* t);
 extern "C" int32_t blend_internal_merge_nsrc(const blend_tree* t);
 extern "C" int32_t blend_internal_dense_ctas(const blend_tree* t);
+extern "C" int32_t blend_internal_max_page(const blend_tree* t);
 
 namespace blend {
 cudaError_t launch_generic(const AttnParams& p, cudaStream_t st);
 cudaError_t launch_merge(const AttnParams& p, cudaStream_t st, bool pdl);
-cudaError_t launch_stream(const AttnParams& p, int64_t n_cache_pages, cudaStream_t st, bool overlap);
 cudaError_t launch_streamw(const AttnParams& p, int64_t n_cache_pages, cudaStream_t st, bool overlap);
 cudaError_t launch_dense(const AttnParams& p, int64_t n_cache_pages, cudaStream_t st);
 }  // namespace blend
 
-static unsigned long long* g_trace = nullptr;   // diagnostics: dense-kernel timeline stamps
+// Diagnostics (blend_internal_set_trace / _set_stats): per-thread so that callers
+// driving several devices from several threads do not share them.
+static thread_local unsigned long long* g_trace = nullptr;   // timeline stamps
+static thread_local unsigned long long* g_stats = nullptr;   // softmax path counters
 extern "C" int blend_internal_set_trace(void* dev) {
   g_trace = (unsigned long long*)dev;
   return 0;
 }
-
-static bool blockIdx_trace_ok(int) { return true; }
+extern "C" int blend_internal_set_stats(void* dev) {
+  g_stats = (unsigned long long*)dev;
+  return 0;
+}
 
 namespace {
 int cuda_fail(cudaError_t e) { return blend_internal_fail(BLEND_ECUDA, cudaGetErrorString(e)); }
@@ -62,10 +66,6 @@ extern "C" int blend_plan_upload(const blend_tree* tree, void* dev_buf, size_t b
     plan->off[i] = off[i];
     plan->count[i] = count[i];
   }
-  plan->count[blend::SEC_COUNT] = blend_internal_partial_rows(tree);
-  plan->count[blend::SEC_COUNT + 1] = blend_internal_stream_entries(tree);
-  plan->count[blend::SEC_COUNT + 2] = blend_internal_merge_unfused(tree);
-  plan->off[blend::SEC_COUNT] = blend_internal_merge_nsrc(tree);   // (off[] past the sections: plan scalars)
   int32_t dims[5];
   blend_internal_tree_dims(tree, dims);
   plan->num_q_heads = dims[0];
@@ -73,7 +73,11 @@ extern "C" int blend_plan_upload(const blend_tree* tree, void* dev_buf, size_t b
   plan->head_dim = dims[2];
   plan->kv_dtype = dims[3];
   plan->page_size = dims[4];
-  plan->reserved = blend_internal_dense_ctas(tree);
+  plan->dense_ctas = blend_internal_dense_ctas(tree);
+  plan->n_partial_rows = blend_internal_partial_rows(tree);
+  plan->stream_entries = blend_internal_stream_entries(tree);
+  plan->merge_nsrc = blend_internal_merge_nsrc(tree);
+  plan->max_page = blend_internal_max_page(tree);
   return BLEND_OK;
 }
 
@@ -84,18 +88,23 @@ extern "C" int blend_attention(const blend_attn_args* a, void* stream) {
   const blend_plan& pl = *a->plan;
   if (!pl.dev) return blend_internal_fail(BLEND_EINVAL, "attention: plan not uploaded");
   if (a->path < 0 || a->path > 2) return blend_internal_fail(BLEND_EINVAL, "attention: bad path");
-  if (a->flags & ~(BLEND_SERIALIZE | BLEND_ARRIVAL_MERGE)) return blend_internal_fail(BLEND_EINVAL, "attention: bad flags");
-  static int arch_ok = -1;
-  if (arch_ok < 0) arch_ok = check_arch() == BLEND_OK ? 1 : 0;
-  if (!arch_ok) return blend_internal_fail(BLEND_EUNSUPPORTED, "libblend is built for sm_100a (B200)");
-  const int64_t prow = pl.count[SEC_COUNT];
+  if (a->flags & ~BLEND_SERIALIZE) return blend_internal_fail(BLEND_EINVAL, "attention: bad flags");
+  if (a->dtype != pl.kv_dtype) return blend_internal_fail(BLEND_EINVAL, "attention: dtype differs from the plan's kv_dtype");
+  if (a->n_cache_pages <= 0 || pl.max_page >= a->n_cache_pages)
+    return blend_internal_fail(BLEND_EINVAL, "attention: the plan reads a page id >= n_cache_pages");
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return cuda_fail(cudaGetLastError());
+  static int arch_ok[64];   // per device: 0 unknown, 1 sm_100, -1 other
+  if (dev < 64 && arch_ok[dev] == 0) arch_ok[dev] = check_arch() == BLEND_OK ? 1 : -1;
+  if (dev >= 64 ? check_arch() != BLEND_OK : arch_ok[dev] < 0)
+    return blend_internal_fail(BLEND_EUNSUPPORTED, "libblend is built for sm_100a (B200)");
+  const int64_t prow = pl.n_partial_rows;
   const int hq = pl.num_q_heads, D = pl.head_dim;
-  size_t o_bytes = ((size_t)prow * hq * D * 4 + 255) & ~size_t(255);
+  const size_t o_bytes = ((size_t)prow * hq * D * 4 + 255) & ~size_t(255);
   const size_t lse_bytes = ((size_t)prow * hq * 4 + 255) & ~size_t(255);
-  const size_t need = o_bytes + 2 * lse_bytes + 256;   // + unit counter + arrival counters [prow][Hq]
+  const size_t need = o_bytes + lse_bytes + 256;   // + the streaming pass's unit counter
   if (!a->workspace || a->workspace_bytes < need)
     return blend_internal_fail(BLEND_ENOSPC, "attention: workspace too small");
-  if (a->n_cache_pages <= 0) return blend_internal_fail(BLEND_EINVAL, "attention: n_cache_pages");
 
   const char* base = (const char*)pl.dev;
   AttnParams p{};
@@ -113,9 +122,7 @@ extern "C" int blend_attention(const blend_attn_args* a, void* stream) {
   p.partmap = (const int32_t*)(base + pl.off[SEC_PARTMAP]);
   p.merge_tok = (const int32_t*)(base + pl.off[SEC_MERGE_TOK]);
   p.merge_off = (const int32_t*)(base + pl.off[SEC_MERGE_OFF]);
-  p.merge_rows = (const int32_t*)(base + pl.off[SEC_MERGE_ROWS]);
   p.srows = (const RowDesc*)(base + pl.off[SEC_STREAM_ROWS]);
-  p.prow_list = (const int32_t*)(base + pl.off[SEC_PROW_LIST]);
   p.dqtok = (const int32_t*)(base + pl.off[SEC_DENSE_QTOK]);
   p.n_tokens = (int32_t)pl.count[SEC_TOK_POS];
   p.n_merge = (int32_t)pl.count[SEC_MERGE_TOK];
@@ -126,13 +133,12 @@ extern "C" int blend_attention(const blend_attn_args* a, void* stream) {
   p.ps = pl.page_size;
   p.kv_f32 = pl.kv_dtype == BLEND_F32;
   p.scale_log2 = kLog2e / sqrtf((float)D);
+  p.stats = g_stats;
   cudaStream_t st = (cudaStream_t)stream;
   const bool generic = a->path == BLEND_PATH_GENERIC || p.kv_f32;
-  const int64_t n_merge_all = pl.count[SEC_MERGE_TOK], n_merge_unfused = pl.count[SEC_COUNT + 2];
   // PDL overlap of the independent dense and streaming passes, unless serialisation is
-  // requested, per-pass events are wanted, or fused merges read dense partials
-  const bool overlap = !generic && !(a->flags & BLEND_SERIALIZE) && !a->events[1] && !a->events[2] &&
-                       n_merge_all == n_merge_unfused;
+  // requested or per-pass events are wanted
+  const bool overlap = !generic && !(a->flags & BLEND_SERIALIZE) && !a->events[1] && !a->events[2];
   cudaError_t e;
 
   if (a->events[0]) cudaEventRecord((cudaEvent_t)a->events[0], st);
@@ -142,17 +148,10 @@ extern "C" int blend_attention(const blend_attn_args* a, void* stream) {
   // The streaming pass hands out units through a counter in the workspace.  The tcgen05
   // dense kernel zeroes it before its launch trigger (so the overlapped streaming grid
   // sees 0); without that kernel a memset ahead of the passes does.
-  const bool stream_dyn = !generic && pl.count[SEC_STREAM_UNITS] > 0 && n_merge_all == n_merge_unfused;
+  const bool stream_dyn = !generic && pl.count[SEC_STREAM_UNITS] > 0;
   const bool dense_tc = !generic && a->path != BLEND_PATH_NO_TCGEN05 && pd.n_units > 0;
-  // Arrival merging (opt-in): when every partial is produced by the tcgen05 dense kernel
-  // or the warp streaming kernel, the last producer of each (token, head) merges it and
-  // the merge launch disappears (no grid-completion dependency at the end of the step).
-  const bool arrival = (a->flags & BLEND_ARRIVAL_MERGE) && !generic && n_merge_all == n_merge_unfused &&
-                       (pd.n_units == 0 || a->path != BLEND_PATH_NO_TCGEN05);
-  int32_t* arrive = arrival ? (int32_t*)((char*)a->workspace + o_bytes + lse_bytes + 256) : nullptr;
-  pd.arrive = arrive;
   pd.trace = g_trace;
-  pd.dense_ctas = overlap ? pl.reserved : 0;   // the cap only makes room for the overlapped streaming grid
+  pd.dense_ctas = overlap ? pl.dense_ctas : 0;   // the cap only makes room for the overlapped streaming grid
   pd.sched = stream_dyn && dense_tc ? p.sched : nullptr;
   if (stream_dyn && !dense_tc) {
     e = cudaMemsetAsync(p.sched, 0, sizeof(int32_t), st);
@@ -166,23 +165,18 @@ extern "C" int blend_attention(const blend_attn_args* a, void* stream) {
   AttnParams ps_ = p;
   ps_.units = (const Unit*)(base + pl.off[SEC_STREAM_UNITS]);
   ps_.n_units = (int32_t)pl.count[SEC_STREAM_UNITS];
-  ps_.avg_entries = ps_.n_units > 0 ? (int32_t)(pl.count[SEC_COUNT + 1] / ps_.n_units) : 0;
-  ps_.arrive = arrive;
-  ps_.trace = blockIdx_trace_ok(ps_.n_units) ? g_trace : nullptr;
+  ps_.avg_entries = ps_.n_units > 0 ? (int32_t)(pl.stream_entries / ps_.n_units) : 0;
+  ps_.trace = g_trace;
   if (generic) e = launch_generic(ps_, st);
-  else if (n_merge_all != n_merge_unfused) e = launch_stream(ps_, a->n_cache_pages, st, overlap);   // fused merges
   else e = launch_streamw(ps_, a->n_cache_pages, st, overlap);
   if (e != cudaSuccess) return cuda_fail(e);
 
   if (a->events[2]) cudaEventRecord((cudaEvent_t)a->events[2], st);
   AttnParams pm = p;
-  pm.n_merge = (int32_t)pl.count[SEC_COUNT + 2];   // fused lists are merged by the streaming pass
   pm.trace = g_trace;
-  pm.merge_nsrc = (int32_t)pl.off[SEC_COUNT];
-  if (!arrival) {
-    e = launch_merge(pm, st, overlap);
-    if (e != cudaSuccess) return cuda_fail(e);
-  }
+  pm.merge_nsrc = pl.merge_nsrc;
+  e = launch_merge(pm, st, overlap);
+  if (e != cudaSuccess) return cuda_fail(e);
   if (a->events[3]) cudaEventRecord((cudaEvent_t)a->events[3], st);
   e = cudaPeekAtLastError();
   if (e != cudaSuccess) return cuda_fail(e);

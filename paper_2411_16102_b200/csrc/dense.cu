@@ -360,29 +360,6 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
     uint32_t sb = 0;                                  // blocks of this tile processed so far
     uint32_t scnt0 = 0, scnt1 = 0;                    // s_full completions consumed per S buffer (registers)
     int2 enext[EPB];                                  // {pos0, count} of the next block's entries
-    // Arrival merging, deferred by one unit: this thread's partial row of the previous
-    // unit (first row of its list, sources, q head, out row) counts in at the next
-    // epilogue; rows whose count-in is the last are merged 8 at a time, 4 lanes each.
-    int pf = -1, pn = 0, ph = 0, pq = 0;
-    auto settle = [&]() {
-      if (__any_sync(0xffffffffu, pf >= 0)) {
-        fence_acq_rel_gpu();   // release: every lane's partial stores before the count-in
-        __syncwarp();
-        const bool last = pf >= 0 && arrive_last(p, pf, ph, pn);
-        uint32_t lm = __ballot_sync(0xffffffffu, last);
-        const int gi = lane >> 2;
-        while (lm) {
-          const int cnt = __popc(lm);
-          const int src = gi < cnt ? (int)__fns(lm, 0, gi + 1) : 0;
-          const int f = __shfl_sync(0xffffffffu, pf, src), n = __shfl_sync(0xffffffffu, pn, src);
-          const int h = __shfl_sync(0xffffffffu, ph, src), q = __shfl_sync(0xffffffffu, pq, src);
-          if (gi < cnt) merge_row4<D>(p, f, n, h, q, lane & 3);
-#pragma unroll 1
-          for (int k = 0; k < 8 && lm; ++k) lm &= lm - 1;
-        }
-      }
-      pf = -1;
-    };
     auto load_meta = [&](const Unit& un, int j) {
 #pragma unroll
       for (int i = 0; i < EPB; ++i) {   // one 8-byte load per entry, no branch (padding: count 0)
@@ -417,13 +394,9 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       // softmax: its P rows only feed its own (never stored) O rows, so they may hold
       // anything; it keeps the barrier protocol
       const bool warp_pad = __all_sync(0xffffffffu, !row_ok);
-      int2 am = make_int2(-1, 0);                     // {merge list, sources} of a partial row
       load_meta(u, 0);
       for (int j = 0; j < nb; ++j, ++sb) {
         const int buf = j & 1;
-        // arrival-merge metadata, loaded during the unit's last block (used after its PV)
-        if (j == nb - 1 && p.arrive != nullptr && tgt >= 0)
-          am = *reinterpret_cast<const int2*>(p.prow_list + 2 * tgt);
         const uint32_t col_s = t * 128 + buf * DN_KB;
         // key positions of this block from the stage metadata the producer wrote (the
         // stage cannot be refilled before this block's P is consumed)
@@ -444,6 +417,29 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         }
         ptx::mbar_wait(&s_full[t * 2 + buf], (buf ? scnt1++ : scnt0++) & 1);   // per-buffer completion count
         ptx::tc_fence_after();
+        // Entries with count < BOX (a node's last page, padding entries): their V rows past
+        // the count may hold anything, NaN included, and the PV MMA would multiply them by
+        // P = 0 -> tile A's warpgroup zeroes them before its P hand-off (the PV MMAs of both
+        // tiles are issued after it).  K rows past the count only reach masked scores.
+        if (t == 0) {
+          bool part = false;
+#pragma unroll
+          for (int i = 0; i < EPB; ++i) part = part || ecur[i].y < BOX;
+          if (part) {
+            uint8_t* vst = smem + L.stage0 + (sb % NS) * L.stage_stride + CH * DN_KCHUNK;
+#pragma unroll
+            for (int i = 0; i < EPB; ++i) {
+              const int nz = BOX - ecur[i].y;
+              for (int x = r; x < nz * CH * 8; x += 128) {
+                const int row = ecur[i].y + x / (CH * 8), c = (x / 8) % CH, k16 = x % 8;
+                *reinterpret_cast<uint4*>(vst + c * DN_KCHUNK + (i * BOX + row) * 128 + k16 * 16) =
+                    make_uint4(0, 0, 0, 0);
+              }
+            }
+            ptx::fence_proxy_async_smem();   // generic stores -> visible to the tensor core (PV)
+            if (r == 0) stat_add(p, STAT_TAIL_ZEROED, 1);
+          }
+        }
 #if BLEND_TRACE_BLOCKS
         if (threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 8 + 2 * j);
 #endif
@@ -499,11 +495,11 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
           exps(m_ref == -INFINITY ? 0.f : m_ref);   // -inf: a padding row (all scores masked)
           slow = __any_sync(0xffffffffu, !(lsum <= 256.f));
         }
-#if BLEND_TRACE_UNITS
-        if (p.trace != nullptr && lane == 0) {   // diagnostics: blocks per path (fast / slow)
-          atomicAdd(p.trace + 296 * 64 + 8 + (slow ? 1 : 0), 1ull);
+        if (p.stats != nullptr && lane == 0) {   // diagnostics: blocks per softmax path
+          stat_add(p, STAT_DENSE_BLOCKS, 1);
+          if (slow) stat_add(p, STAT_DENSE_SLOW, 1);
+          if (slow && j > 0) stat_add(p, STAT_DENSE_SLOW_LATE, 1);
         }
-#endif
         if (slow) {
         float mxv[8];
 #pragma unroll
@@ -515,6 +511,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         const float mx2 = mx * p.scale_log2;
         const bool need = mx2 > m_ref + DN_RESCALE_T;
         if (j > 0 && __any_sync(0xffffffffu, need)) {
+          if (lane == 0) stat_add(p, STAT_DENSE_RESCALE, 1);
           // O holds PV up to block j-1: wait for it.  Parity is unambiguous because the
           // previous completion on this barrier (PV(j-3)) is certified by s_full(j-1) and
           // PV(j+1) cannot be issued before this block's P.
@@ -564,7 +561,6 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       const float m_use = m_ref == -INFINITY ? 0.f : m_ref;
       const float inv = l > 0.f ? 1.f / l : 0.f;
       const float lse2 = l > 0.f ? m_use + log2f(l) : -INFINITY;
-      if (p.arrive != nullptr) settle();   // the previous unit's partial rows (stores long complete)
       // O / l leaves through a per-warp smem staging tile (XOR-swizzled 16-B units, no
       // bank conflicts), so that every global store instruction writes whole 128-B row
       // segments (4 rows per instruction) instead of 32 scattered 16-B pieces.
@@ -646,19 +642,12 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       if (threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 61);
       if (tgt == PM_DIRECT) p.lse[(int64_t)token * p.hq + head] = lse2 * kLn2;
       else if (tgt >= 0) p.ws_lse[(int64_t)tgt * p.hq + head] = lse2;
-      if (p.arrive != nullptr && tgt >= 0) {   // counts in at the next unit's epilogue (or the end)
-        pf = am.x;
-        pn = am.y;
-        ph = head;
-        pq = token * p.hq + head;
-      }
       ptx::tc_fence_before();
       if (threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 5);
 #if BLEND_TRACE_UNITS
       if (threadIdx.x == 128 && uk < 10) trace_stamp(p, 21 + 2 * uk);
 #endif
     }
-    if (p.arrive != nullptr) settle();
   }
   __syncwarp();       // lane 0 of the producer / MMA warps rejoins its warp before the CTA barrier
   ptx::tc_fence_before();

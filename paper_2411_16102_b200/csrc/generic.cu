@@ -27,13 +27,6 @@ constexpr int GEN_KT = 32;
 __device__ __forceinline__ void write_row(const AttnParams& p, const RowInfo& ri, int32_t tgt, const float* o,
                                           float inv_l, float lse2, int lane_stride, int lane) {
   if (tgt == PM_SKIP) return;
-  if (tgt <= PM_FUSED_BASE) {
-    float ov[16];
-    const int n = (p.d - lane + lane_stride - 1) / lane_stride;   // elements lane, lane+32, ...
-    for (int k = 0; k < n; ++k) ov[k] = o[lane + k * lane_stride] * inv_l;
-    fused_merge_store(p, tgt, ri.token, ri.head, ov, lse2, lane, lane_stride, n, lane == 0);
-    return;
-  }
   if (tgt == PM_DIRECT) {
     int64_t base = ((int64_t)ri.token * p.hq + ri.head) * p.d;
     for (int e = lane; e < p.d; e += lane_stride) st_elem(p.out, base + e, o[e] * inv_l, p.kv_f32);

@@ -101,9 +101,9 @@ struct blend_tree {
   size_t workspace_bytes = 0;
   int64_t n_partial_rows = 0;
   int64_t stream_entries = 0;   // sum over stream units of their entry counts (launch heuristic)
-  int32_t n_merge_unfused = 0;  // merge lists [0, n) are merged by the merge kernel
   int32_t dense_ctas = 0;       // dense-pass grid cap (0: one CTA per SM), set by the planner
-  int32_t merge_nsrc = 0;       // > 0: every unfused merge list has this many sources
+  int32_t merge_nsrc = 0;       // > 0: every merge list has this many sources
+  int32_t max_page = -1;        // largest physical page id in page_table (-1: no pages)
 };
 
 namespace {
@@ -126,7 +126,7 @@ int validate(const blend_build_args* a) {
     return fail(BLEND_EINVAL, "page_size must be a power of two in [16,128]");
   if (a->kv_dtype != BLEND_BF16 && a->kv_dtype != BLEND_F32) return fail(BLEND_EINVAL, "kv_dtype");
   if (a->rows_min < 0 || a->min_sep_len < -1 || a->force_class < 0 || a->force_class > 2 ||
-      a->split_tokens < 0 || a->num_sms < 0 || a->dense_split < 0 || a->fuse_merge < 0 || a->fuse_merge > 1)
+      a->split_tokens < 0 || a->num_sms < 0 || a->dense_split < 0)
     return fail(BLEND_EINVAL, "rows_min/min_sep_len/force_class/split_tokens/num_sms");
   if (a->n_req < 1) return fail(BLEND_EINVAL, "n_req must be >= 1");
   if (!a->tok_off || !a->tokens || !a->q_len || !a->prompt_len || !a->out_len)
@@ -396,6 +396,8 @@ int build_descriptors(blend_tree* t) {
     if (npages > INT32_MAX) return fail(BLEND_ENOSPC, "too many pages");
     for (int64_t i = 0; i < npages; ++i) t->page_table[i] = (int32_t)i;
   }
+  t->max_page = -1;
+  for (int32_t pg : t->page_table) t->max_page = std::max(t->max_page, pg);
 
   // ---- 6. request paths, classes
   const int32_t g = a.num_q_heads / a.num_kv_heads;
@@ -673,7 +675,6 @@ int build_plan(blend_tree* t) {
   std::vector<int32_t> nsrc(T, 0);
   struct Src {
     int32_t tok, key_start, pm;
-    bool dense;
   };
   std::vector<Src> srcs;
   for (size_t ii = 0; ii < items.size(); ++ii) {
@@ -684,7 +685,7 @@ int build_plan(blend_tree* t) {
         int32_t tk = it.toks[i];
         if (ks <= tok_pos[tk]) {
           nsrc[tk] += 1;
-          srcs.push_back({tk, ks, pm_base[ii][s] + (int32_t)i, it.dense});
+          srcs.push_back({tk, ks, pm_base[ii][s] + (int32_t)i});
         }
       }
     }
@@ -694,50 +695,29 @@ int build_plan(blend_tree* t) {
   std::stable_sort(srcs.begin(), srcs.end(), [](const Src& x, const Src& y) {
     return x.tok != y.tok ? x.tok < y.tok : x.key_start < y.key_start;
   });
-  // Merge lists, ascending key start.  A token whose only streaming source is a
-  // single (item, split) and whose other sources are all dense-pass partials is
-  // merged by that streaming unit itself ("fused"): the dense pass has completed
-  // on the stream before the streaming pass starts.  Its list holds -1 for the
-  // streaming unit's own in-register result; fused tokens follow the unfused ones.
-  struct Group {
-    size_t i, j;
-    bool fused;
-  };
-  std::vector<Group> groups;
+  // Merge lists, ascending key start (reading #17): list m holds the partial rows
+  // merge_off[m] .. merge_off[m+1]-1 in that order, so the merge kernel reads partial
+  // row s for list entry s without an index lookup.
+  std::vector<int32_t> merge_tok, merge_off{0};
+  int64_t prow = 0;
   for (size_t i = 0; i < srcs.size();) {
     size_t j = i;
-    int n_stream = 0;
-    while (j < srcs.size() && srcs[j].tok == srcs[i].tok) n_stream += srcs[j++].dense ? 0 : 1;
-    if (j - i == 1) partmap[srcs[i].pm] = blend::PM_DIRECT;
-    else groups.push_back({i, j, a.fuse_merge != 0 && n_stream == 1});
+    while (j < srcs.size() && srcs[j].tok == srcs[i].tok) ++j;
+    if (j - i == 1) {
+      partmap[srcs[i].pm] = blend::PM_DIRECT;
+    } else {
+      merge_tok.push_back(srcs[i].tok);
+      for (size_t k = i; k < j; ++k) partmap[srcs[k].pm] = (int32_t)prow++;
+      merge_off.push_back((int32_t)prow);
+    }
     i = j;
   }
-  std::vector<int32_t> merge_tok, merge_off{0}, merge_rows;
-  int64_t prow = 0;
-  int32_t n_unfused = 0;
-  for (int pass = 0; pass < 2; ++pass)
-    for (const Group& gr : groups) {
-      if (gr.fused != (pass == 1)) continue;
-      const int32_t m = (int32_t)merge_tok.size();
-      merge_tok.push_back(srcs[gr.i].tok);
-      for (size_t k = gr.i; k < gr.j; ++k) {
-        if (gr.fused && !srcs[k].dense) {
-          partmap[srcs[k].pm] = blend::PM_FUSED_BASE - m;
-          merge_rows.push_back(-1);
-        } else {
-          partmap[srcs[k].pm] = (int32_t)prow;
-          merge_rows.push_back((int32_t)prow++);
-        }
-      }
-      merge_off.push_back((int32_t)merge_rows.size());
-      if (pass == 0) ++n_unfused;
-    }
-  t->n_merge_unfused = n_unfused;
+  const int32_t n_merge = (int32_t)merge_tok.size();
   t->merge_nsrc = 0;
-  if (n_unfused > 0) {
+  if (n_merge > 0) {
     const int32_t n0 = merge_off[1] - merge_off[0];
     bool uni = true;
-    for (int32_t m = 1; m < n_unfused && uni; ++m) uni = merge_off[m + 1] - merge_off[m] == n0;
+    for (int32_t m = 1; m < n_merge && uni; ++m) uni = merge_off[m + 1] - merge_off[m] == n0;
     if (uni) t->merge_nsrc = n0;
   }
   if (prow > INT32_MAX / 2) return fail(BLEND_EINVAL, "too many partial rows");
@@ -806,36 +786,17 @@ int build_plan(blend_tree* t) {
   // kernel gets each row's q/out row, position and partmap target in one load
   // instead of the item_tokens -> tok_pos / partmap chain.
   std::vector<blend::RowDesc> srows(sunits.size() * blend::STREAM_ROWS,
-                                    blend::RowDesc{-1, INT32_MIN, blend::PM_SKIP, -1, -1, 0, 0, 0});
-  // partial row -> {first partial row of its merge list, the list's source count}.  An
-  // unfused list's entries are its partial rows in order (merge_rows[s] == s: rows are
-  // allocated in list order above), so neither the merge kernel nor an arrival-merging
-  // producer needs further lookups.
-  std::vector<int32_t> prow_list(2 * prow, -1);
-  for (size_t m = 0; m < (size_t)n_unfused; ++m)
-    for (int32_t s_ = merge_off[m]; s_ < merge_off[m + 1]; ++s_) {
-      if (merge_rows[s_] != s_)   // the merge kernel reads partial row s of entry s directly
-        return fail(BLEND_EINVAL, "internal: merge list %zu not in partial-row order", m);
-      prow_list[2 * merge_rows[s_]] = merge_rows[merge_off[m]];
-      prow_list[2 * merge_rows[s_] + 1] = merge_off[m + 1] - merge_off[m];
-    }
-  {
-    const int32_t g = a.num_q_heads / a.num_kv_heads;
-    for (size_t ui = 0; ui < sunits.size(); ++ui) {
-      const blend::Unit& u = sunits[ui];
-      for (int r = 0; r < u.n_rows; ++r) {
-        const int32_t ir = u.row_begin + r, tl = ir / g, j = ir % g;
-        const int32_t tok = item_tokens[u.tok_base + tl];
-        blend::RowDesc& d = srows[ui * blend::STREAM_ROWS + r];
-        d.qrow = tok * a.num_q_heads + u.kvh * g + j;
-        d.pos = tok_pos[tok];
-        d.target = partmap[u.pm_base + tl];
-        d.head = u.kvh * g + j;
-        if (d.target >= 0) {
-          d.first = prow_list[2 * d.target];
-          d.nsrc = prow_list[2 * d.target + 1];
-        }
-      }
+                                    blend::RowDesc{-1, INT32_MIN, blend::PM_SKIP, -1});
+  for (size_t ui = 0; ui < sunits.size(); ++ui) {
+    const blend::Unit& u = sunits[ui];
+    for (int r = 0; r < u.n_rows; ++r) {
+      const int32_t ir = u.row_begin + r, tl = ir / g, j = ir % g;
+      const int32_t tok = item_tokens[u.tok_base + tl];
+      blend::RowDesc& d = srows[ui * blend::STREAM_ROWS + r];
+      d.qrow = tok * a.num_q_heads + u.kvh * g + j;
+      d.pos = tok_pos[tok];
+      d.target = partmap[u.pm_base + tl];
+      d.head = u.kvh * g + j;
     }
   }
 
@@ -859,18 +820,15 @@ int build_plan(blend_tree* t) {
   put(SEC_PARTMAP, partmap.data(), 4, partmap.size());
   put(SEC_MERGE_TOK, merge_tok.data(), 4, merge_tok.size());
   put(SEC_MERGE_OFF, merge_off.data(), 4, merge_off.size());
-  put(SEC_MERGE_ROWS, merge_rows.data(), 4, merge_rows.size());
   put(SEC_STREAM_ROWS, srows.data(), sizeof(RowDesc), srows.size());
-  put(SEC_PROW_LIST, prow_list.data(), 4, prow_list.size());
   put(SEC_DENSE_QTOK, dqtok.data(), 4, dqtok.size());
   blob.resize((blob.size() + 255) & ~size_t(255));
 
   t->n_partial_rows = prow;
   const size_t hq = a.num_q_heads, D = a.head_dim;
   size_t o_bytes = ((size_t)prow * hq * D * 4 + 255) & ~size_t(255);
-  // partials o | lse | unit counter (256 B) | arrival counters [partial row][Hq] (the
-  // counter of a list is the one of its first row)
-  t->workspace_bytes = o_bytes + 2 * (((size_t)prow * hq * 4 + 255) & ~size_t(255)) + 256;
+  // partials o | lse | unit counter of the streaming pass (256 B)
+  t->workspace_bytes = o_bytes + (((size_t)prow * hq * 4 + 255) & ~size_t(255)) + 256;
   t->info.n_tokens = T;
   t->info.n_items = (int64_t)items.size();
   t->info.n_dense_units = (int64_t)dunits.size();
@@ -1105,7 +1063,7 @@ int blend_internal_fail(int status, const char* msg) { return fail(status, "%s",
 
 int64_t blend_internal_partial_rows(const blend_tree* t) { return t ? t->n_partial_rows : 0; }
 int64_t blend_internal_stream_entries(const blend_tree* t) { return t ? t->stream_entries : 0; }
-int64_t blend_internal_merge_unfused(const blend_tree* t) { return t ? t->n_merge_unfused : 0; }
+int32_t blend_internal_max_page(const blend_tree* t) { return t ? t->max_page : -1; }
 int32_t blend_internal_dense_ctas(const blend_tree* t) { return t ? t->dense_ctas : 0; }
 int32_t blend_internal_merge_nsrc(const blend_tree* t) { return t ? t->merge_nsrc : 0; }
 

@@ -15,10 +15,9 @@ enum PlanSection {
   SEC_STREAM_UNITS,    // Unit[n_stream]
   SEC_PARTMAP,         // int32[]    per (item, split) x item token: partial row | DIRECT | SKIP
   SEC_MERGE_TOK,       // int32[M]   tokens with >= 2 sources
-  SEC_MERGE_OFF,       // int32[M+1]
-  SEC_MERGE_ROWS,      // int32[]    partial rows, ascending key-range start (-1 = the fusing unit)
+  SEC_MERGE_OFF,       // int32[M+1] list m = partial rows merge_off[m] .. merge_off[m+1]-1, ascending
+                       //            key-range start (reading #17)
   SEC_STREAM_ROWS,     // RowDesc[n_stream * STREAM_ROWS]  per-row descriptors of the streaming units
-  SEC_PROW_LIST,       // int32[2P]  {first partial row of its merge list, source count} (arrival merging)
   SEC_DENSE_QTOK,      // int32[n_dense]  first token of a dense unit whose tokens are consecutive
                        //                 (its Q tiles load by TMA boxes), else -1
   SEC_COUNT
@@ -26,7 +25,6 @@ enum PlanSection {
 
 constexpr int32_t PM_DIRECT = -1;   // the only source of this token: write out/lse directly
 constexpr int32_t PM_SKIP = -2;     // this (item, split) has no key at or before the token
-constexpr int32_t PM_FUSED_BASE = -3;  // <= -3: streaming unit merges list m = PM_FUSED_BASE - value itself
 
 // One KV page entry: <= 64 consecutive slots of one physical page.
 struct KvEntry {
@@ -54,12 +52,8 @@ struct Unit {
 struct RowDesc {
   int32_t qrow;      // token * Hq + q head: row of q / out / lse
   int32_t pos;       // absolute position of the token (causal bound)
-  int32_t target;    // partmap value: partial row | PM_DIRECT | PM_SKIP | fused
+  int32_t target;    // partmap value: partial row | PM_DIRECT | PM_SKIP
   int32_t head;      // q head (partial-row column)
-  int32_t first;     // partial row: first partial row of its merge list (rows first .. first+nsrc-1,
-                     // ascending key start); -1 for DIRECT / SKIP.  Arrival counter first * Hq + head
-  int32_t nsrc;      // sources of that list
-  int32_t pad0, pad1;
 };
 
 constexpr int DENSE_ROWS = 256;    // rows per dense unit: two 128-row tcgen05 Q tiles (UMMA M=128)

@@ -253,26 +253,6 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
     ptx::cp_async_commit();
   };
 
-  // Arrival merging, deferred by one unit: the rows of the unit before count in (and
-  // the last source of a (token, head) merges it, 4 lanes per row) once this warp has
-  // streamed another unit.
-  RowDesc pend0{-1, 0, PM_SKIP, 0, -1, 0, 0, 0}, pend1 = pend0;
-  auto settle = [&]() {
-    const bool any = (pend0.qrow >= 0 && pend0.target >= 0) || (pend1.qrow >= 0 && pend1.target >= 0);
-    if (__any_sync(0xffffffffu, any)) {
-      fence_acq_rel_gpu();   // release: every lane's partial stores before the count-in
-      __syncwarp();
-#pragma unroll
-      for (int half_row = 0; half_row < 2; ++half_row) {
-        const RowDesc d = half_row ? pend1 : pend0;
-        bool last = false;
-        if (c4 == 0 && d.qrow >= 0 && d.target >= 0) last = arrive_last(p, d.first, d.head, d.nsrc);
-        last = __shfl_sync(0xffffffffu, last, lane & ~3);
-        if (last) merge_row4<D>(p, d.first, d.nsrc, d.head, d.qrow, c4);
-      }
-    }
-    pend0.qrow = pend1.qrow = -1;
-  };
   int4 nann = next_index();
   Pre pre{};
   if (nann.x < p.n_units) {
@@ -323,6 +303,20 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
         const int nvalid = en_count - kbase;           // >= 1
         ptx::mbar_wait(&wfull[s], ph);
         if (warp == 0 && lane == 0 && k == 0 && h == 0) trace_stamp_s(p, 3 + 4 * tu);
+        // A partial stage loads whole 16-row groups: the V rows past the entry's count
+        // (the tail of a node's last page) may hold anything, NaN included, and the PV
+        // MMA multiplies them by P = 0 -> zero them (the K rows are masked by the select
+        // below, which discards NaN scores).
+        const bool tail = nvalid < SW_KEYS && (nvalid & 15) != 0;
+        if (tail) {
+          const int nz = 16 - (nvalid & 15);
+          uint8_t* vz = ring + s * L.stage_stride + CH * SW_CHUNK + nvalid * 128;
+          for (int u = lane; u < nz * CH * 8; u += 32) {
+            const int row = u / (CH * 8), c = (u / 8) % CH, k16 = u % 8;
+            *reinterpret_cast<uint4*>(vz + c * SW_CHUNK + row * 128 + k16 * 16) = make_uint4(0, 0, 0, 0);
+          }
+          __syncwarp();
+        }
 #if BLEND_TRACE_STAGES
         if (warp == 0 && lane == 0 && it >= 4 && it < 12) trace_stamp_s(p, 36 + (it - 4));
 #endif
@@ -366,6 +360,15 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
         mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
         const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
         const float mu0 = mn0 == -INFINITY ? 0.f : mn0, mu1 = mn1 == -INFINITY ? 0.f : mn1;
+        if (p.stats != nullptr) {   // diagnostics: stages, and stages that rescale a live row's O
+          const bool rs = (m0 != -INFINITY && mn0 > m0) || (m1 != -INFINITY && mn1 > m1);
+          const bool any_rs = __any_sync(0xffffffffu, rs);
+          if (lane == 0) {
+            stat_add(p, STAT_STREAM_STAGES, 1);
+            if (any_rs) stat_add(p, STAT_STREAM_RESCALE, 1);
+            if (tail) stat_add(p, STAT_TAIL_ZEROED, 1);
+          }
+        }
         const float al0 = ptx::ex2(m0 - mu0), al1 = ptx::ex2(m1 - mu1);
         m0 = mn0;
         m1 = mn1;
@@ -407,6 +410,7 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
             ptx::mma_bf16_16816(o[j + 1], pa, b2, b3);
           }
         }
+        if (tail) ptx::fence_proxy_async_smem();   // generic zero stores before the next TMA write
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&wempty[s]);
 #if BLEND_TRACE_STAGES
@@ -420,9 +424,6 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
     }
     if (q_pending) issue_q(pre, buf ^ 1);
     if (warp == 0 && lane == 0) trace_stamp_s(p, 4 + 4 * tu);
-    // ---- unit end: the previous unit's partial rows count in (their stores are long
-    // complete, so the release fence is cheap), then this unit's rows are written
-    if (p.arrive != nullptr) settle();
     // ---- unit end: rows g8 (o[.][0,1]) and g8+8 (o[.][2,3]) straight from the fragments
     l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
     l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
@@ -451,13 +452,8 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
         if (c4 == 0) p.ws_lse[(int64_t)d.target * p.hq + d.head] = lse2;
       }
     }
-    if (p.arrive != nullptr) {   // this unit's partial rows count in at the next unit's end
-      pend0 = cu.d0;
-      pend1 = cu.d1;
-    }
     if (warp == 0 && lane == 0) trace_stamp_s(p, 5 + 4 * tu);
   }
-  if (p.arrive != nullptr) settle();
   ptx::pdl_wait();
 }
 

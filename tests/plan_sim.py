@@ -16,7 +16,7 @@ from oracle import attention as A
 from synth import values as V
 
 SEC = ["tok_pos", "item_tok_off", "item_tokens", "entries", "dunits", "sunits", "partmap",
-       "merge_tok", "merge_off", "merge_rows", "stream_rows", "prow_list", "dense_qtok"]
+       "merge_tok", "merge_off", "stream_rows", "dense_qtok"]
 
 
 def plan_image(tree):
@@ -31,13 +31,12 @@ def plan_image(tree):
     blob = np.ctypeslib.as_array(C.cast(data, C.POINTER(C.c_uint8)), (nbytes.value,)).copy() \
         if nbytes.value else np.zeros(0, np.uint8)
     secs = {}
-    width = {"entries": 4, "dunits": 8, "sunits": 8, "stream_rows": 8}
+    width = {"entries": 4, "dunits": 8, "sunits": 8, "stream_rows": 4}
     for i, name in enumerate(SEC):
         o, n = int(off[i]), int(cnt[i])
         k = width.get(name, 1)
         secs[name] = blob[o:o + 4 * n * k].view(np.int32).reshape(n, k) if k > 1 else \
             blob[o:o + 4 * n].view(np.int32)
-    secs["prow_list"] = secs["prow_list"].reshape(-1, 2)
     return secs
 
 
@@ -49,22 +48,17 @@ def check_stream_rows(P, g, Hq):
     token, head, position, partmap target) exactly."""
     sr = P["stream_rows"]
     assert len(sr) == STREAM_ROWS * len(P["sunits"])
-    mo = P["merge_off"]
     for ui, u in enumerate(P["sunits"]):
         item, kvh, rb, nr, eb, ee, pmb, tb = (int(x) for x in u)
         for r in range(STREAM_ROWS):
-            qrow, pos, tgt, head, first, ns = (int(x) for x in sr[ui * STREAM_ROWS + r][:6])
+            qrow, pos, tgt, head = (int(x) for x in sr[ui * STREAM_ROWS + r])
             if r >= nr:
-                assert qrow == -1 and tgt == -2 and first == -1
+                assert qrow == -1 and tgt == -2
                 continue
             tl, j = (rb + r) // g, (rb + r) % g
             tok = int(P["item_tokens"][tb + tl])
             assert (qrow, pos, tgt, head) == (tok * Hq + kvh * g + j, int(P["tok_pos"][tok]),
                                               int(P["partmap"][pmb + tl]), kvh * g + j)
-            if tgt >= 0:   # arrival merging: the row's list is rows first .. first + ns - 1
-                assert first <= tgt < first + ns
-            else:
-                assert first == -1
 
 
 def check_dense_qtok(P, g):
@@ -101,8 +95,6 @@ def simulate(w, tree):
     out = np.full((T, Hq, D), np.nan)
     lse = np.full((T, Hq), np.nan)
     written = np.zeros((T, Hq), dtype=np.int64)
-    fused = {}
-    dense_rows = set()
     check_stream_rows(P, g, Hq)
     check_dense_qtok(P, g)
     for kind, units in (("dense", P["dunits"]), ("stream", P["sunits"])):
@@ -128,41 +120,21 @@ def simulate(w, tree):
                 tgt = int(P["partmap"][pmb + tl])
                 if tgt == -2:
                     continue
-                if tgt <= -3:                       # fused: this unit merges list m itself
-                    fused[(tok, head)] = (o[0, 0], l[0, 0])
-                    continue
                 if tgt == -1:
                     out[tok, head], lse[tok, head] = o[0, 0], l[0, 0]
                     written[tok, head] += 1
                 else:
                     assert np.isnan(part_l[tgt, head]), "partial row written twice"
                     part_o[tgt, head], part_l[tgt, head] = o[0, 0], l[0, 0]
-                    if kind == "dense":
-                        dense_rows.add(tgt)
     mo = P["merge_off"]
-    pl = P["prow_list"]
-    assert len(pl) == nprow
+    assert int(mo[-1]) == nprow
     for m, tok in enumerate(P["merge_tok"]):
-        rows = P["merge_rows"][mo[m]:mo[m + 1]]
-        if all(r >= 0 for r in rows):   # arrival merging: consecutive rows, each knows the list
-            assert list(rows) == list(range(int(rows[0]), int(rows[0]) + len(rows)))
-            for r in rows:
-                assert tuple(int(x) for x in pl[r]) == (int(rows[0]), len(rows))
-        real = [r for r in rows if r >= 0]
-        assert not np.isnan(part_l[real]).any(), "merge reads an unwritten partial"
-        assert sum(1 for r in rows if r < 0) <= 1
-        if any(r < 0 for r in rows):          # fused by a streaming unit: only dense-pass partials
-            assert all(r in dense_rows for r in real), "fused list reads a streaming partial"
+        rows = list(range(int(mo[m]), int(mo[m + 1])))   # list m = partial rows mo[m] .. mo[m+1]-1
+        assert len(rows) >= 2
+        assert not np.isnan(part_l[rows]).any(), "merge reads an unwritten partial"
         for h in range(Hq):
-            parts = []
-            for r in rows:
-                if r >= 0:
-                    parts.append((part_o[r, h][None, None], part_l[r, h][None, None]))
-                else:
-                    fo, fl = fused.pop((int(tok), h))
-                    parts.append((fo[None, None], np.array([[fl]])))
+            parts = [(part_o[r, h][None, None], part_l[r, h][None, None]) for r in rows]
             O, L = A.lse_merge(parts)
             out[tok, h], lse[tok, h] = O[0, 0], L[0, 0]
         written[tok] += 1
-    assert not fused, "fused results never merged"
     return out, lse, written, P

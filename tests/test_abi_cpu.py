@@ -29,7 +29,7 @@ def test_exports_every_header_symbol():
     L = B.lib()
     for n in sorted(names):
         assert hasattr(L, n), n
-    assert L.blend_abi_version() == 1
+    assert L.blend_abi_version() == 2
 
 
 def _same(v_c, v_o):
