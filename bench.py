@@ -1,20 +1,25 @@
 #!/usr/bin/env python
 """bench.py — blended-batch attention tokens/s on B200 (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c3|c5|c1b_bf16|...]
-                    [--impl ours|reference] [--path auto|generic|no_tcgen05]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c4|c4_t0.8|...|c2|c3|c5]
+                    [--impl ours|reference] [--path auto|generic|no_tcgen05] [--weak] [--tp]
 
 One step = one blend_attention call (dense tcgen05 pass + streaming pass + LSE
 merge) over the whole blended batch of the workload, one layer, inputs resident
-in HBM.  Default workload = configs[1] (C2: Llama-3.1-8B shapes, decode batch
-256 over a shared ~1K MMLU-like prefix).  Its working set (113 MB) fits in L2,
-so L2 is flushed (256 MB write) between timed steps.
+in HBM.  Default workload = configs[3] (C4: the 40,000-request synthetic grid
+workload at compute density t = 1.0 and prefix sharing ratio 0.5, Llama-3.1-8B
+shapes; 66 GB of KV per layer, far larger than L2, so no flush is needed).
+Other configs are parity cases and extra lines (c2 / c3 / c5; c4_t0.8..1.4 is the
+density sweep).
 
-N > 1 (torchrun): weak scaling — the global batch is N independent copies of the
-recipe (distinct system prompts); every rank builds the global tree, blend_shard
-splits it 2N-block-fold into N subtree shards, each rank runs its shard.  No KV
-crosses GPUs; NCCL only all-reduces the timings (max over ranks) and, outside
-the timed region, all-gathers the outputs.
+N > 1 (torchrun): strong scaling of ONE global batch — every rank builds the global
+tree, blend_shard splits it into N subtree shards "from both sides", each rank
+fills and runs only its shard (no KV crosses GPUs); NCCL all-reduces the timings
+(max over ranks) and, outside the timed region, all-gathers out + lse, which rank 0
+re-assembles in global request order and checks against the whole batch run on one
+GPU.  --weak: N independent copies of the recipe instead.  --tp: head-parallel ranks
+(NEXT-4): each rank takes Hkv/N kv heads of the whole batch, outputs gathered along
+the head axis.
 
 --impl reference: the fp64 oracle (oracle/attention.py) on the host cores, on a
 bounded sample of the same workload each step (the paper publishes no attention
@@ -54,7 +59,7 @@ def load_peaks():
     return d
 
 
-PROFILE_TAG = "r1h"   # profiles/<tag>_ncu.json: ncu --set full captures of this code's kernels
+PROFILE_TAG = "r2a"   # profiles/<tag>_ncu.json: ncu --set full captures of this code's kernels
 
 
 def ncu_traffic(workload: str, kernel: str):
@@ -73,7 +78,8 @@ def ncu_traffic(workload: str, kernel: str):
 
 def make_workload(name: str, n_copies: int = 1):
     from synth import workloads as W
-    recipes = {"c2": (W.c2_mmlu_decode, 2), "c3": (W.c3_burst_openvid, 3), "c5": (W.c5_70b_32k, 5)}
+    recipes = {"c2": (W.c2_mmlu_decode, 2), "c3": (W.c3_burst_openvid, 3), "c5": (W.c5_70b_32k, 5),
+               "c4": (W.c4_grid, 4)}
     if name in recipes:
         fn, seed = recipes[name]
         if n_copies == 1:
@@ -233,12 +239,33 @@ def run_reference(args):
     return 0
 
 
+def _roofline(kind, pw, t_ms, peaks, burst, workload, path_auto):
+    """Roofline entry of one pass: algorithmic work per launch / its event-timed duration."""
+    if kind == "dense":
+        tf = pw["dense_flops"] / (t_ms * 1e-3) / 1e12 if t_ms > 0 else 0.0
+        peak = peaks["bf16_tflops"] if burst else peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+        traffic, tsrc = ncu_traffic(workload, "dense_kernel") if path_auto else (None, None)
+        return {"kernel": "dense_kernel (tcgen05)" if path_auto else "dense (generic executor)",
+                "bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak,
+                "traffic": traffic, "traffic_source": tsrc, "launch_ms": t_ms,
+                "algorithmic_per_launch": pw["dense_flops"], "algorithmic_bytes_per_launch": pw["dense_bytes"],
+                "peak_source": peaks["_source"] + (" bf16 burst" if burst else " bf16 sustained")}
+    gbs = pw["stream_bytes"] / (t_ms * 1e-3) / 1e9 if t_ms > 0 else 0.0
+    peak = peaks["hbm_gbs"]
+    traffic, tsrc = ncu_traffic(workload, "streamw_kernel") if path_auto else (None, None)
+    return {"kernel": "streamw_kernel", "bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s",
+            "frac": gbs / peak, "traffic": traffic, "traffic_source": tsrc, "launch_ms": t_ms,
+            "algorithmic_per_launch": pw["stream_bytes"], "peak_source": peaks["_source"] + " HBM copy"}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
+    from dataclasses import replace as _replace
 
     import paper_2411_16102_b200 as B
-    from harness.run import build_tree, device_batch, pass_work, subset, work_counts
+    from harness.dp import gather_heads, gather_rows, shard_batch, tp_heads
+    from harness.run import device_batch, pass_work, work_counts
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -254,25 +281,23 @@ def run_ours(args):
                    dense_split=args.dense_split, split_tokens=args.split_tokens)
 
     t0 = time.perf_counter()
+    req_shard = None
     if args.tp:
-        # NEXT-4: head-parallel replicas — every rank runs the whole
-        # batch for its Hkv/N kv heads and their query-head groups (no exchange inside
-        # attention); strong scaling of one batch.  Synthetic values use local head indices.
-        from dataclasses import replace as _replace
+        # NEXT-4: head-parallel ranks — rank k takes kv heads
+        # [k Hkv/N, (k+1) Hkv/N) and their query-head groups for the whole batch, with
+        # global head indices in the synthetic values; strong scaling of one batch.
         gw = make_workload(args.workload, 1)
-        tpn = args.tp_ranks if args.tp_ranks else world   # --tp-ranks: one rank's slice of a wider TP group
-        if gw.num_kv_heads % tpn:
-            raise SystemExit(f"--tp: {gw.num_kv_heads} kv heads do not split over {tpn} ranks")
-        w = _replace(gw, num_q_heads=gw.num_q_heads // tpn, num_kv_heads=gw.num_kv_heads // tpn,
+        tpn = args.tp_ranks if args.tp_ranks else world   # --tp-ranks: one rank's slice of a wider group
+        hq, hkv, h0, kvh0 = tp_heads(gw, tpn, rank if world > 1 else 0)
+        w = _replace(gw, num_q_heads=hq, num_kv_heads=hkv, head0=h0, kv_head0=kvh0,
                      name=f"{gw.name}_tp{tpn}_rank{rank}")
+        mode = "tp"
     else:
-        gw = make_workload(args.workload, world)
-        if world > 1:
-            gtree = build_tree(gw, **tree_kw)
-            req_shard, _ = gtree.shard(world)
-            w = subset(gw, np.nonzero(req_shard == rank)[0], name=f"{gw.name}_shard{rank}")
-        else:
-            w = gw
+        # data parallelism by subtree shards: one global batch
+        # split across the ranks (strong scaling); --weak: N independent copies
+        gw = make_workload(args.workload, world if args.weak else 1)
+        w, req_shard, _ = shard_batch(gw, world, rank, tree_kw)
+        mode = "weak" if args.weak else "dp"
     db = device_batch(w, tree_kw=tree_kw)
     host_s = time.perf_counter() - t0
     view = db.view
@@ -280,14 +305,20 @@ def run_ours(args):
     pw = pass_work(w, view)
     info = db.info
     stream = torch.cuda.current_stream()
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    do_flush = not args.no_flush
+    # L2 (126 MB): KV working sets within a few x L2 are flushed between timed steps; larger
+    # ones are their own flush (every step streams > 4 x L2 of distinct KV)
+    L2_BYTES = 126 << 20
+    do_flush = not args.no_flush and KVb < 4 * L2_BYTES
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if do_flush else None
 
     for _ in range(args.warmup):
+        if do_flush:
+            B.l2_flush(flush)
         db.run(path=path)
     torch.cuda.synchronize()
 
     K = args.steps
+
     def mk_events(n, m):
         evs = [[torch.cuda.Event(enable_timing=True) for _ in range(m)] for _ in range(n)]
         for row in evs:       # torch creates CUDA events lazily: materialise the handles
@@ -295,9 +326,9 @@ def run_ours(args):
                 e.record(stream)
         return evs
 
-    # ---- timed region: K whole steps (dense || streaming via PDL, then merge), events at the ends
+    # ---- timed region: K whole steps (dense || streaming via PDL, then merge), events on the
+    # launching stream around each blend_attention call
     ev = mk_events(K, 2)
-    # ---- per-pass breakdown: K serialised steps with events between the passes (roofline)
     evp = mk_events(K, 4)
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
@@ -314,6 +345,8 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
+    # ---- per-pass breakdown (rooflines): K more steps with BLEND_SERIALIZE and events between
+    # the passes (the dense grid then spans every SM)
     for k in range(K):
         if do_flush:
             B.l2_flush(flush)
@@ -330,31 +363,30 @@ def run_ours(args):
     tok = torch.tensor([float(w.sum_q)], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(loc, op=dist.ReduceOp.MAX)
-        if not args.tp:   # TP: every rank works on the same tokens (its share of the heads)
+        if mode != "tp":   # TP: every rank works on the same tokens (its share of the heads)
             dist.all_reduce(tok, op=dist.ReduceOp.SUM)
     ms, md, mst, mm, mser = loc.tolist()
     total_tok = tok.item()
     value = total_tok / (ms * 1e-3)
 
-    # ---- e2e through the public API: every step copies its Q in from pinned host memory
-    # and its out + lse back.  Copies run on their own streams, double-buffered, so step
-    # k's device->host read overlaps step k+1's attention and step k+2's host->device copy
-    # (events order each buffer set: H2D -> attention -> D2H -> next H2D into the set).
+    # ---- e2e through the public API with host buffers: every step copies its Q in from
+    # pinned host memory (side stream), calls blend_attention, and copies out + lse back
+    # (side stream); NB buffer sets let step k's download overlap step k+1's attention.
+    # No device head start: the host's enqueue cost (Python, ctypes, argument checks,
+    # tensor-map lookups) is inside the events.
+    io_bytes = 2 * db.q.numel() * db.q.element_size()
+    K_e2e = K if io_bytes < (1 << 30) else min(K, 6)
     q_host = torch.empty(db.q.shape, dtype=db.q.dtype, pin_memory=True)
     q_host.copy_(db.q)
-    io_bytes = 2 * db.q.numel() * db.q.element_size()
-    NB = 4 if io_bytes < (256 << 20) else 2   # buffer sets in flight
+    NB = 4 if io_bytes < (256 << 20) else 2
     out_host = [torch.empty(db.out.shape, dtype=db.out.dtype, pin_memory=True) for _ in range(NB)]
     lse_host = [torch.empty(db.lse.shape, dtype=db.lse.dtype, pin_memory=True) for _ in range(NB)]
     qd = [db.q] + [torch.empty_like(db.q) for _ in range(NB - 1)]
     od = [db.out] + [torch.empty_like(db.out) for _ in range(NB - 1)]
     ld = [db.lse] + [torch.empty_like(db.lse) for _ in range(NB - 1)]
-    # L2: a flush kernel on the compute stream would sit inside this timed region, so the
-    # e2e steps instead use inputs larger than L2 — KV caches under 256 MB are rotated
-    # over 3 copies (each step's cache was last touched two steps earlier, with >= 2x its
-    # size of other traffic in between)
-    kv_bytes = 2 * db.k_cache.numel() * db.k_cache.element_size()
-    nrot = 3 if kv_bytes < (256 << 20) else 1
+    # L2: small KV caches rotate over 3 copies (each step's cache was last touched two steps
+    # earlier, with >= 2x its size of other traffic in between) instead of a flush kernel
+    nrot = 3 if KVb < 4 * L2_BYTES else 1
     kc = [db.k_cache] + [db.k_cache.clone() for _ in range(nrot - 1)]
     vc = [db.v_cache] + [db.v_cache.clone() for _ in range(nrot - 1)]
     s_h2d, s_d2h = torch.cuda.Stream(), torch.cuda.Stream()
@@ -363,13 +395,12 @@ def run_ours(args):
     ev_d2h = [torch.cuda.Event() for _ in range(NB)]
     e2e_t0, e2e_t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
-    # head start: the device sleeps (outside the timed region) while the host enqueues the
-    # K steps, so the events time the device pipeline, not the Python loop that feeds it
-    torch.cuda._sleep(int(2.0e9 * max(2e-3, K * 150e-6)))
+    if world > 1:
+        dist.barrier()
     e2e_t0.record(stream)
     s_h2d.wait_event(e2e_t0)
     s_d2h.wait_event(e2e_t0)
-    for k in range(K):
+    for k in range(K_e2e):
         b = k % NB
         with torch.cuda.stream(s_h2d):
             if k >= NB:
@@ -385,62 +416,61 @@ def run_ours(args):
             out_host[b].copy_(od[b], non_blocking=True)
             lse_host[b].copy_(ld[b], non_blocking=True)
             ev_d2h[b].record(s_d2h)
-    for b in range(min(K, NB)):
+    for b in range(min(K_e2e, NB)):
         stream.wait_event(ev_d2h[b])
     e2e_t1.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = torch.tensor([e2e_t0.elapsed_time(e2e_t1) / K], dtype=torch.float64, device="cuda")
+    e2e_ms = torch.tensor([e2e_t0.elapsed_time(e2e_t1) / K_e2e], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_ms = e2e_ms.item()
     h2d = db.q.numel() * db.q.element_size()
     d2h = db.out.numel() * db.out.element_size() + db.lse.numel() * db.lse.element_size()
     # the copied-back result of the last step equals the device result of the same input
-    e2e_match = bool(torch.equal(out_host[(K - 1) % NB], od[0].cpu()))
+    e2e_match = bool(torch.equal(out_host[(K_e2e - 1) % NB], od[(K_e2e - 1) % NB].cpu()))
+    del q_host, out_host, lse_host, qd[1:], od[1:], ld[1:], kc[1:], vc[1:]
 
-    # ---- output gather over NVLink (timed separately, not in the metric)
-    gather_ms = None
+    # ---- outputs and LSE rows gathered over NVLink (NCCL), re-assembled in global request
+    # order on rank 0 (timed separately: DP ranks keep their outputs, SURVEY d-5) and checked
+    # against the whole batch run on one GPU (the G-GPU == 1-GPU invariant, §8(e))
+    gather_ms, dp_check = None, None
     if world > 1:
-        rows = torch.tensor([db.out.shape[0]], device="cuda")
-        dist.all_reduce(rows, op=dist.ReduceOp.MAX)
-        pad = torch.zeros((int(rows.item()),) + tuple(db.out.shape[1:]), dtype=db.out.dtype, device="cuda")
-        pad[:db.out.shape[0]] = db.out
-        allo = torch.empty((world,) + tuple(pad.shape), dtype=pad.dtype, device="cuda")
         g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         dist.barrier()
         g0.record()
-        dist.all_gather_into_tensor(allo, pad)
+        if mode == "tp":
+            of, lf = gather_heads(db.out, db.lse, world, dist)
+        else:
+            of, lf = gather_rows(db.out, db.lse, gw, req_shard, world, dist)
         g1.record()
         torch.cuda.synchronize()
         gather_ms = g0.elapsed_time(g1)
+        if rank == 0 and not args.no_check:
+            del db
+            torch.cuda.empty_cache()
+            full = device_batch(gw, tree_kw=tree_kw)
+            full.run(path=path)
+            torch.cuda.synchronize()
+            dp_check = {"vs": "the unsharded batch on one GPU (G-GPU == 1-GPU, SURVEY §8(e))",
+                        "out_max_abs": float((of.float() - full.out.float()).abs().max().item()),
+                        "lse_max_abs": float((lf - full.lse).abs().max().item()),
+                        "rows": int(of.shape[0]), "tol": "2e-2 (bf16 north-star atol; different plans)"}
+            dp_check["ok"] = dp_check["out_max_abs"] <= 2e-2 and dp_check["lse_max_abs"] <= 1e-3
+            del full
+        dist.barrier()
 
-    # our kernels per timed step: dense + streaming (+ merge: only off the arrival-merge
-    # path, i.e. the generic executor) + the L2 flush between steps
-    arrival = False   # BLEND_ARRIVAL_MERGE is opt-in; the bench runs the default path
+    # our kernels per timed step: dense + streaming + merge (+ the L2 flush between steps)
     launches_per_step = int(info["n_dense_units"] > 0) + int(info["n_stream_units"] > 0) + \
-        int(info["n_merge_tokens"] > 0 and not arrival) + int(do_flush)
+        int(info["n_merge_tokens"] > 0) + int(do_flush)
 
-    # ---- roofline of the dominant kernel (per launch, CUDA events on the launching stream)
+    # ---- rooflines of both passes (per launch, CUDA events on the launching stream)
     peaks = load_peaks()
     burst = ms < 100.0
-    if md >= mst:
-        tf = pw["dense_flops"] / (md * 1e-3) / 1e12
-        peak = peaks["bf16_tflops"] if burst else peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
-        traffic, tsrc = ncu_traffic(args.workload, "dense_kernel") if path == B.PATH_AUTO else (None, None)
-        roof = {"kernel": "dense (tcgen05)" if path == B.PATH_AUTO else "dense (generic executor)",
-                "bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak,
-                "traffic": traffic, "traffic_source": tsrc, "algorithmic_per_launch": pw["dense_flops"],
-                "algorithmic_bytes_per_launch": pw["dense_bytes"],
-                "peak_source": peaks["_source"] + (" burst" if burst else " sustained")}
-    else:
-        gbs = pw["stream_bytes"] / (mst * 1e-3) / 1e9
-        peak = peaks["hbm_gbs"]
-        traffic, tsrc = ncu_traffic(args.workload, "streamw_kernel") if path == B.PATH_AUTO else (None, None)
-        roof = {"kernel": "stream", "bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s",
-                "frac": gbs / peak, "traffic": traffic, "traffic_source": tsrc,
-                "algorithmic_per_launch": pw["stream_bytes"], "peak_source": peaks["_source"]}
+    path_auto = path == B.PATH_AUTO
+    roofs = {"dense": _roofline("dense", pw, md, peaks, burst, args.workload, path_auto),
+             "stream": _roofline("stream", pw, mst, peaks, burst, args.workload, path_auto)}
+    dominant = "dense" if md >= mst else "stream"
 
-    line = None
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
@@ -449,42 +479,50 @@ def run_ours(args):
             except Exception as e:  # noqa: BLE001
                 cpu = {"value": None, "unit": "tokens/s", "cores": len(os.sched_getaffinity(0)),
                        "kind": "oracle", "sample": f"failed: {e}"}
+        par = {"tp": f"tp{world} (kv heads)" if world > 1 else
+               (f"one rank of tp{args.tp_ranks} (kv heads)" if args.tp_ranks else "tp1 (kv heads)"),
+               "dp": f"dp{world} (subtree shards of one batch)" if world > 1 else "single GPU",
+               "weak": f"dp{world} (subtree shards of {world} independent copies)"}[mode]
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong" if args.tp else "weak",
+            "scaling": "weak" if mode == "weak" else "strong",
             "vs_baseline": None, "dtype": "bf16" if w.kv_dtype == "bf16" else "f32", "data": "synthetic",
             "config": {"workload": gw.name, "requests": gw.n_req, "query_tokens": int(total_tok),
                        "heads": f"{gw.num_q_heads}/{gw.num_kv_heads}x{gw.head_dim}"
-                                + (f" (per rank {w.num_q_heads}/{w.num_kv_heads})" if args.tp else ""),
-                       "page_size": w.page_size,
-                       "parallelism": (f"tp{world} (kv heads)" if args.tp else f"dp{world} (subtree shards)")
-                       if world > 1 else ((f"one rank of tp{args.tp_ranks} (kv heads)" if args.tp_ranks
-                                           else "tp1 (kv heads)") if args.tp else "single GPU"),
-                       "l2": "flushed (256 MB write) between timed steps" if do_flush else "not flushed",
+                                + (f" (per rank {w.num_q_heads}/{w.num_kv_heads})" if mode == "tp" else ""),
+                       "page_size": w.page_size, "parallelism": par,
+                       "l2": "flushed (256 MB write) between timed steps" if do_flush else
+                             f"inputs larger than L2 (KV {KVb / 1e9:.1f} GB per rank), no flush",
                        "path": args.path},
             "clocks": clk,
             "e2e": {"value": total_tok / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
-                    "note": "blend_attention with Q copied in from pinned host memory and out + lse copied "
-                            "back every step; copies on side streams, NB buffer sets (step k's D2H "
-                            "overlaps step k+1's attention and step k+2's upload)", "buffer_sets": NB, "output_matches_device": e2e_match,
-                    "l2": (f"KV rotated over {nrot} copies ({nrot * kv_bytes >> 20} MB > L2), no flush in the "
-                           "timed region" if nrot > 1 else "inputs larger than L2, no flush in the timed region")},
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms, "steps": K_e2e,
+                    "note": "blend_attention through the Python binding with Q copied in from pinned host "
+                            "memory and out + lse copied back every step (side streams, NB buffer sets); "
+                            "the host's enqueue cost is inside the timed region",
+                    "buffer_sets": NB, "output_matches_device": e2e_match,
+                    "l2": (f"KV rotated over {nrot} copies, no flush in the timed region" if nrot > 1
+                           else "inputs larger than L2, no flush in the timed region")},
             "gpu_launches": launches_per_step * K,
-            "roofline": roof,
+            "roofline": roofs[dominant],
+            "rooflines": roofs,
             "cpu_baseline": cpu,
             "passes_ms": {"dense": md, "stream": mst, "merge": mm, "serialized_step": mser,
                           "note": "per-pass times from K extra steps run with BLEND_SERIALIZE (dense grid on "
                                   "every SM); the timed steps overlap the dense and streaming passes (PDL), "
                                   "with the dense grid capped by the planner when both passes are large"},
             "work": {"F_alg": F, "B_alg": Bytes, "kv_bytes": KVb, **pw,
-                     "whole_step_roofline_frac_measured": max(F / (load_peaks()["bf16_tflops"] * 1e12),
-                                                              Bytes / (load_peaks()["hbm_gbs"] * 1e9)) / (ms * 1e-3)},
+                     "whole_step_roofline_frac_measured": max(F / (peaks["bf16_tflops"] * 1e12),
+                                                              Bytes / (peaks["hbm_gbs"] * 1e9)) / (ms * 1e-3)},
             "plan": info,
             "host_build_s": host_s,
             "gather_ms": gather_ms,
+            "dp_check": dp_check,
         }
+        if "t" in gw.meta:
+            line["config"]["density_t"] = gw.meta["t"]
+            line["config"]["counts_burst_openvid_mmlu"] = list(gw.meta["counts"])
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -497,13 +535,18 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="c2")
+    ap.add_argument("--workload", default="c4",
+                    help="c4 (= c4_t1.0) | c4_t0.8 | c4_t1.2 | c4_t1.4 | c2 | c3 | c5 | c1*_bf16 ...")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--path", default="auto", choices=["auto", "generic", "no_tcgen05"])
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--dense-split", type=int, default=0, help="dense split-KV factor (0 = planner auto)")
     ap.add_argument("--split-tokens", type=int, default=0, help="streaming split-KV chunk (0 = auto)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--weak", action="store_true",
+                    help="N > 1: N independent copies of the recipe (weak scaling) instead of one batch")
+    ap.add_argument("--no-check", action="store_true",
+                    help="N > 1: skip rank 0's check of the gathered result against the 1-GPU run")
     ap.add_argument("--tp", action="store_true",
                     help="head-parallel replicas (NEXT-4): each rank takes Hkv/N kv heads of the whole batch")
     ap.add_argument("--tp-ranks", type=int, default=0,

@@ -105,10 +105,10 @@ def device_batch(w, device="cuda", tree_kw=None, n_cache_pages=None, fill=True) 
         pid, pcnt, phash = page_slot_hashes(w, view)
         B.fill_kv(k_cache, v_cache, w.kv_dtype, w.num_kv_heads, w.head_dim, w.page_size,
                   torch.from_numpy(pid).to(device), torch.from_numpy(pcnt).to(device),
-                  torch.from_numpy(phash.view(np.int64)).to(device), w.seed)
+                  torch.from_numpy(phash.view(np.int64)).to(device), w.seed, kv_head0=w.kv_head0)
         gid, tt = query_rows(w)
         B.fill_q(q, w.kv_dtype, w.num_q_heads, w.head_dim, torch.from_numpy(gid).to(device),
-                 torch.from_numpy(tt).to(device), w.seed, w.scale_q)
+                 torch.from_numpy(tt).to(device), w.seed, w.scale_q, head0=w.head0)
     torch.cuda.synchronize()
     return DeviceBatch(w, tree, view, plan, q, k_cache, v_cache, out, lse, ws, ncp, build_s,
                        tree.plan_info())
@@ -142,7 +142,8 @@ def subset(w, reqs, name=None):
                     layers=w.layers,
                     tokens=np.concatenate(paths).astype(np.int32) if paths else np.zeros(0, np.int32),
                     tok_off=tok_off, q_len=w.q_len[reqs], prompt_len=w.prompt_len[reqs],
-                    out_len=w.out_len[reqs], scale_q=w.scale_q, global_id=gid)
+                    out_len=w.out_len[reqs], scale_q=w.scale_q, global_id=gid, head0=w.head0,
+                    kv_head0=w.kv_head0)
 
 
 def pass_work(w, view, rows_min=128, force_class=0):

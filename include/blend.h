@@ -236,19 +236,22 @@ int blend_attention(const blend_attn_args* args, void* stream);
 /* ------------------------------------------------------------------------ */
 /* Synthetic input fillers (bench / tests; SURVEY.md §8(c-7) generator).      */
 /* ------------------------------------------------------------------------ */
-/* K/V cache fill: for i < n_pages, page page_ids[i] slot s < page_count[i] gets
- * KV[kvh][e] = grid(mix(page_hash[i*ps+s] ^ mix(seed_kv + ((kind*2^8 + kvh)*2^12 + e))))
+/* K/V cache fill: for i < n_pages, page page_ids[i] slot s < page_count[i] gets, for the
+ * cache's kv head k < num_kv_heads (global kv head kvh = kv_head0 + k: a head-parallel
+ * rank's slice keeps the full problem's values),
+ * KV[k][e] = grid(mix(page_hash[i*ps+s] ^ mix(seed_kv + ((kind*2^8 + kvh)*2^12 + e))))
  * with seed_kv = seed ^ 0x5BD1E9955BD1E995; slots >= page_count[i] are zeroed.
  * page_ids, page_count, page_hash are DEVICE arrays. */
 int blend_fill_kv(void* k_cache, void* v_cache, int32_t kv_dtype, int32_t num_kv_heads,
-                  int32_t head_dim, int32_t page_size, const int32_t* page_ids,
+                  int32_t kv_head0, int32_t head_dim, int32_t page_size, const int32_t* page_ids,
                   const int32_t* page_count, const uint64_t* page_hash, int64_t n_pages,
                   uint64_t seed, void* stream);
 
-/* Q fill: row i gets Q[h][e] = scale_q * grid(mix(seed_q ^ mix(((gid*2^20 + t)*2^8 + h)*2^12 + e)))
+/* Q fill: row i, q head k < num_q_heads (global head h = head0 + k) gets
+ * Q[k][e] = scale_q * grid(mix(seed_q ^ mix(((gid*2^20 + t)*2^8 + h)*2^12 + e)))
  * (all arithmetic mod 2^64; kind 0 = K, 1 = V; grid(z) = ((z>>56) - 128) / 128)
  * with gid = row_gid[i], t = row_t[i], seed_q = seed ^ 0xC2B2AE3D27D4EB4F.  DEVICE arrays. */
-int blend_fill_q(void* q, int32_t dtype, int32_t num_q_heads, int32_t head_dim,
+int blend_fill_q(void* q, int32_t dtype, int32_t num_q_heads, int32_t head0, int32_t head_dim,
                  const int64_t* row_gid, const int32_t* row_t, int64_t n_rows, uint64_t seed,
                  float scale_q, void* stream);
 

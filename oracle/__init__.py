@@ -1,8 +1,9 @@
 """Oracle: plain, slow, obviously-correct CPU reference for the blended-batch
 tree attention hot path (arXiv 2411.16102, BlendServe).
 
-TEST INFRASTRUCTURE ONLY.  Only `tests/`, `__graft_entry__.smoke()` and
-`bench.py`'s cpu_baseline / `--impl reference` legs may import anything here.
+TEST INFRASTRUCTURE ONLY.  Only `tests/`, `__graft_entry__.smoke()`,
+`bench.py`'s cpu_baseline / `--impl reference` legs and the committed scripts that
+write stored expected values (`scripts/solve_c4_counts.py`) may import anything here.
 The product path (`paper_2411_16102_b200`, `libblend.so`) never imports,
 links or executes this package, and this package never imports the product.
 The two share no code; both draw inputs from `synth/` (input generation only).

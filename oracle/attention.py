@@ -81,9 +81,9 @@ def request_inputs(w, r: int):
     """Materialise (K, V, Q) of request r from the synthetic generator (fp64,
     exactly the bf16/fp32 grid values the device sees)."""
     path = w.path(r)
-    K, Vv = V.path_kv(path, w.seed, w.num_kv_heads, w.head_dim)
+    K, Vv = V.path_kv(path, w.seed, w.num_kv_heads, w.head_dim, w.kv_head0)
     q = int(w.q_len[r])
-    Q = V.q_values(w.gid(r), np.arange(q), w.seed, w.num_q_heads, w.head_dim, w.scale_q)
+    Q = V.q_values(w.gid(r), np.arange(q), w.seed, w.num_q_heads, w.head_dim, w.scale_q, w.head0)
     return K, Vv, Q
 
 

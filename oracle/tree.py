@@ -295,3 +295,37 @@ def dump(v, w) -> str:
             v["cu"][i], v["mu"][i], "S" if v["node_class"][i] else "F",
             int(v["node_nreq"][i]), ",".join(str(x) for x in v["node_ends"][i])))
     return "\n".join(lines) + "\n"
+
+
+# ---------------------------------------------------------------------------
+# Density of a request set, hardware constants restored (P:87-96 cost model; P:309-315
+# rho = Comp / Mem, rho(R) = (1 - s) T_comp / T_mem).  Used to check the C4 grid
+# recipe's realised density and sharing and by the committed script
+# that solves its request counts (scripts/solve_c4_counts.py).
+# ---------------------------------------------------------------------------
+def request_key(p: int, d: int, model_params: int, hidden: int, layers: int):
+    """(CU, MU) of ONE request: P:89 Comp numerator (p + d) * P_model * 2 + p^2 * H * L * 4
+    and P:93 Mem's exact sum sum_{i=1..d} (p + i) (hardware constants removed)."""
+    return 2 * model_params * (p + d) + 4 * hidden * layers * p * p, p * d + d * (d + 1) // 2
+
+
+def root_key(view):
+    """(CU, MU) of the whole batch (the virtual root over the forest): top-level subtrees
+    have disjoint closures and request sets, so their keys add."""
+    tops = [i for i in range(view["n_nodes"]) if int(view["node_parent"][i]) < 0]
+    return sum(view["cu"][i] for i in tops), sum(view["mu"][i] for i in tops)
+
+
+def density(cu: int, mu: int, compute: float, bandwidth: float, kv_bytes_per_token: int) -> float:
+    """rho = Comp / Mem = (CU / compute) / (MU * H_kv * L * 4 / bandwidth) (P:89, P:93; the
+    4 = K and V at 2 bytes; reading #8: H_kv = Hkv * D)."""
+    return (cu / compute) / (mu * kv_bytes_per_token / bandwidth) if mu else float("inf")
+
+
+def sharing_ratio(w, view) -> float:
+    """Prefix sharing ratio s of the batch read as the GEMM-token saving (SURVEY §8(d-4),
+    P:141): 1 - CU_all / sum_r CU_r, CU_r the single-request key."""
+    cu_all, _ = root_key(view)
+    tot = sum(request_key(int(w.prompt_len[r]), int(w.out_len[r]), int(w.model_params), int(w.hidden),
+                          int(w.layers))[0] for r in range(w.n_req))
+    return 1.0 - cu_all / tot

@@ -94,9 +94,9 @@ EXPORTS = {
     "blend_workspace_bytes": (C.c_size_t, [C.c_void_p]),
     "blend_plan_upload": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.POINTER(Plan)]),
     "blend_attention": (C.c_int, [C.POINTER(AttnArgs), C.c_void_p]),
-    "blend_fill_kv": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+    "blend_fill_kv": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                 C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_uint64, C.c_void_p]),
-    "blend_fill_q": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
+    "blend_fill_q": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                C.c_int64, C.c_uint64, C.c_float, C.c_void_p]),
     "blend_l2_flush": (C.c_int, [C.c_void_p, C.c_size_t, C.c_void_p]),
 }
@@ -306,16 +306,16 @@ def attention(q, k_cache, v_cache, plan: Plan, out, lse, workspace, *, n_cache_p
 
 
 def fill_kv(k_cache, v_cache, kv_dtype, num_kv_heads, head_dim, page_size, page_ids, page_count,
-            page_hash, seed, stream=None):
+            page_hash, seed, stream=None, kv_head0=0):
     """blend_fill_kv (device arrays page_ids/page_count/page_hash as torch tensors)."""
     _check(lib().blend_fill_kv(k_cache.data_ptr(), v_cache.data_ptr(), _DTYPES.get(kv_dtype, kv_dtype),
-                               num_kv_heads, head_dim, page_size, page_ids.data_ptr(),
+                               num_kv_heads, kv_head0, head_dim, page_size, page_ids.data_ptr(),
                                page_count.data_ptr(), page_hash.data_ptr(), page_ids.numel(),
                                C.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), C.c_void_p(_stream_handle(stream))))
 
 
-def fill_q(q, dtype, num_q_heads, head_dim, row_gid, row_t, seed, scale_q=1.0, stream=None):
-    _check(lib().blend_fill_q(q.data_ptr(), _DTYPES.get(dtype, dtype), num_q_heads, head_dim,
+def fill_q(q, dtype, num_q_heads, head_dim, row_gid, row_t, seed, scale_q=1.0, stream=None, head0=0):
+    _check(lib().blend_fill_q(q.data_ptr(), _DTYPES.get(dtype, dtype), num_q_heads, head0, head_dim,
                               row_gid.data_ptr(), row_t.data_ptr(), row_gid.numel(),
                               C.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), C.c_float(scale_q),
                               C.c_void_p(_stream_handle(stream))))

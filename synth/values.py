@@ -55,36 +55,39 @@ def prefix_hash(tokens: np.ndarray, seed: int) -> np.ndarray:
     return np.bitwise_xor.accumulate(leaf) if leaf.size else leaf
 
 
-def kv_salt_table(seed: int, kind: int, num_kv_heads: int, head_dim: int) -> np.ndarray:
-    """mix(seed_kv + ((kind*2^8 + kvh)*2^12 + e)) as uint64[Hkv, D]."""
+def kv_salt_table(seed: int, kind: int, num_kv_heads: int, head_dim: int, kv_head0: int = 0) -> np.ndarray:
+    """mix(seed_kv + ((kind*2^8 + kvh)*2^12 + e)) as uint64[Hkv, D], kvh = kv_head0 .. +Hkv-1
+    (global kv head indices: a head-parallel slice keeps the full problem's values)."""
     seed_kv = np.uint64((seed ^ KV_SALT) & 0xFFFFFFFFFFFFFFFF)
-    kvh = np.arange(num_kv_heads, dtype=np.uint64)[:, None]
+    kvh = np.arange(kv_head0, kv_head0 + num_kv_heads, dtype=np.uint64)[:, None]
     e = np.arange(head_dim, dtype=np.uint64)[None, :]
     ctr = ((np.uint64(kind) << np.uint64(8)) + kvh) * np.uint64(1 << 12) + e
     with np.errstate(over="ignore"):
         return mix(seed_kv + ctr)
 
 
-def kv_values(h: np.ndarray, seed: int, kind: int, num_kv_heads: int, head_dim: int) -> np.ndarray:
+def kv_values(h: np.ndarray, seed: int, kind: int, num_kv_heads: int, head_dim: int,
+              kv_head0: int = 0) -> np.ndarray:
     """K (kind=0) or V (kind=1) values float64[n, Hkv, D] for prefix hashes h[n]."""
-    salt = kv_salt_table(seed, kind, num_kv_heads, head_dim)
+    salt = kv_salt_table(seed, kind, num_kv_heads, head_dim, kv_head0)
     z = mix(np.asarray(h, dtype=np.uint64)[:, None, None] ^ salt[None, :, :])
     return grid(z)
 
 
-def path_kv(tokens: np.ndarray, seed: int, num_kv_heads: int, head_dim: int):
+def path_kv(tokens: np.ndarray, seed: int, num_kv_heads: int, head_dim: int, kv_head0: int = 0):
     """(K, V) float64[n, Hkv, D] of a full token path."""
     h = prefix_hash(tokens, seed)
-    return (kv_values(h, seed, 0, num_kv_heads, head_dim),
-            kv_values(h, seed, 1, num_kv_heads, head_dim))
+    return (kv_values(h, seed, 0, num_kv_heads, head_dim, kv_head0),
+            kv_values(h, seed, 1, num_kv_heads, head_dim, kv_head0))
 
 
 def q_values(global_req: int, t: np.ndarray, seed: int, num_q_heads: int, head_dim: int,
-             scale_q: float = 1.0) -> np.ndarray:
-    """Q float64[len(t), Hq, D] for query indices t of request `global_req`."""
+             scale_q: float = 1.0, head0: int = 0) -> np.ndarray:
+    """Q float64[len(t), Hq, D] for query indices t of request `global_req`, q heads
+    head0 .. head0+Hq-1 (global head indices)."""
     seed_q = np.uint64((seed ^ Q_SALT) & 0xFFFFFFFFFFFFFFFF)
     t = np.asarray(t, dtype=np.uint64)[:, None, None]
-    h = np.arange(num_q_heads, dtype=np.uint64)[None, :, None]
+    h = np.arange(head0, head0 + num_q_heads, dtype=np.uint64)[None, :, None]
     e = np.arange(head_dim, dtype=np.uint64)[None, None, :]
     with np.errstate(over="ignore"):
         ctr = ((np.uint64(global_req) * np.uint64(1 << 20) + t) * np.uint64(1 << 8) + h) \

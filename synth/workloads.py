@@ -11,6 +11,8 @@ prompt.  Lognormals are parameterised by their MEAN and sigma.
 """
 from __future__ import annotations
 
+import json
+import os
 from dataclasses import dataclass, field, replace
 from typing import List, Optional
 
@@ -44,6 +46,8 @@ class Workload:
     scale_q: float = 1.0
     free_pages: Optional[np.ndarray] = None   # int32 physical page ids, None = 0,1,2,...
     global_id: Optional[np.ndarray] = None    # int64[R] global request index (Q generator)
+    head0: int = 0                            # global index of q head 0 (head-parallel slices)
+    kv_head0: int = 0                         # global index of kv head 0
     meta: dict = field(default_factory=dict)
 
     @property
@@ -161,24 +165,40 @@ def c5_70b_32k(seed: int = 5, n_docs: int = 16, per_doc: int = 64, doc_len: int 
     return _pack("c5_70b_32k", seed, paths, q, p, d, dict(LLAMA70B), "bf16", 64)
 
 
-def c4_grid(seed: int = 4, counts=(18646, 54, 21300), chunk: int = 512) -> Workload:
+C4_COUNTS_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "c4_counts.json")
+C4_T = (0.8, 1.0, 1.2, 1.4)
+
+
+def c4_counts(t: float):
+    """(BurstGPT, OpenVid, MMLU) request counts of the C4 grid at density t: the table
+    written by scripts/solve_c4_counts.py (solved on the realised samples with the
+    oracle's density keys)."""
+    with open(C4_COUNTS_PATH) as f:
+        table = json.load(f)
+    e = table["t"][f"{t:.1f}"]
+    return tuple(int(x) for x in e["counts"])
+
+
+def c4_grid(seed: int = 4, t: float = 1.0, counts=None, chunk: int = 512, n_total: int = 40000) -> Workload:
     """configs[3]: the paper's A.1 grid recipe with synthetic lengths —
     40,000 requests mixing BurstGPT-like (prompt LN(600, 0.7) in [16, 4096], output
     LN(256, 0.7) in [1, 4096]), OpenVid-like (caption LN(100, 0.4) in [16, 512],
-    frames LN(64, 0.3) in [8, 256], d = 256 frames rescaled to mean 16384) and
+    frames LN(64, 0.3) in [8, 256], d = 256 tokens per frame, mean 16384) and
     MMLU-like requests (57 subjects with a 5-shot prefix U{400..1000}, question
     LN(100, 0.4) in [20, 400], d = 2); 3-level tree: trace system prompt (128)
-    -> MMLU subject -> request.  Counts (Burst, OpenVid, MMLU) = SURVEY §8(d-4)'s
-    expected-length solve for compute density t = 1.0 and sharing s = 0.5.
+    -> MMLU subject -> request.  Counts (Burst, OpenVid, MMLU) for compute density t and
+    sharing s = 0.5 come from c4_counts(t) unless given.
+    Each class draws from its own random stream, so the first n requests of a class do
+    not depend on the other classes' counts (the count solve is monotone).
     Snapshot: every request sits at a uniformly random step of its lifetime
     (ceil(p_private / 512) prefill chunks, then d decodes); shared prefixes cached."""
-    rng = np.random.default_rng(seed)
-    nb, nv, nm = counts
-    sys_b, sys_v, sys_m = _toks(rng, 128), _toks(rng, 128), _toks(rng, 128)
-    subj = [_toks(rng, int(rng.integers(400, 1001))) for _ in range(57)]
+    nb, nv, nm = c4_counts(t) if counts is None else counts
+    rs = np.random.default_rng([seed, 0])
+    sys_b, sys_v, sys_m = _toks(rs, 128), _toks(rs, 128), _toks(rs, 128)
+    subj = [_toks(rs, int(rs.integers(400, 1001))) for _ in range(57)]
     paths, q, p, d = [], [], [], []
 
-    def snapshot(shared, priv_len, dd):
+    def snapshot(rng, shared, priv_len, dd):
         n_chunks = -(-priv_len // chunk)
         k = int(rng.integers(0, n_chunks + dd))
         if k < n_chunks:
@@ -190,27 +210,32 @@ def c4_grid(seed: int = 4, counts=(18646, 54, 21300), chunk: int = 512) -> Workl
             qq = 1
         return np.concatenate([shared, priv]), qq
 
-    pb = _lognormal_mean(rng, 600, 0.7, nb, 16, 4096)
-    db = _lognormal_mean(rng, 256, 0.7, nb, 1, 4096)
-    for i in range(nb):
-        path, qq = snapshot(sys_b, int(pb[i]), int(db[i]))
-        paths.append(path); q.append(qq); p.append(128 + int(pb[i])); d.append(int(db[i]))
-    cap = _lognormal_mean(rng, 100, 0.4, nv, 16, 512)
-    frames = _lognormal_mean(rng, 64, 0.3, nv, 8, 256)
-    dv = 256 * frames
-    dv = np.maximum(1, np.rint(dv * (16384.0 / max(1.0, dv.mean())))).astype(np.int64)
-    for i in range(nv):
-        path, qq = snapshot(sys_v, int(cap[i]), int(dv[i]))
-        paths.append(path); q.append(qq); p.append(128 + int(cap[i])); d.append(int(dv[i]))
-    qm = _lognormal_mean(rng, 100, 0.4, nm, 20, 400)
-    sm = rng.integers(0, 57, size=nm)
-    for i in range(nm):
-        shared = np.concatenate([sys_m, subj[int(sm[i])]])
-        path, qq = snapshot(shared, int(qm[i]), 2)
-        paths.append(path); q.append(qq); p.append(len(shared) + int(qm[i])); d.append(2)
-    order = rng.permutation(len(paths))             # arrival order is not tree order
-    return _pack("c4_grid_t1.0_s0.5", seed, [paths[i] for i in order], np.asarray(q)[order],
-                 np.asarray(p)[order], np.asarray(d)[order], dict(LLAMA8B), "bf16", 64)
+    rb = np.random.default_rng([seed, 1])
+    for _ in range(nb):
+        pb = int(_lognormal_mean(rb, 600, 0.7, 1, 16, 4096)[0])
+        db = int(_lognormal_mean(rb, 256, 0.7, 1, 1, 4096)[0])
+        path, qq = snapshot(rb, sys_b, pb, db)
+        paths.append(path); q.append(qq); p.append(128 + pb); d.append(db)
+    rv = np.random.default_rng([seed, 2])
+    # d = 256 tokens per frame; E[frames] = 64 -> mean d = 16384
+    for _ in range(nv):
+        cap = int(_lognormal_mean(rv, 100, 0.4, 1, 16, 512)[0])
+        frames = int(_lognormal_mean(rv, 64, 0.3, 1, 8, 256)[0])
+        dv = 256 * frames
+        path, qq = snapshot(rv, sys_v, cap, dv)
+        paths.append(path); q.append(qq); p.append(128 + cap); d.append(dv)
+    rm = np.random.default_rng([seed, 3])
+    for _ in range(nm):
+        qm = int(_lognormal_mean(rm, 100, 0.4, 1, 20, 400)[0])
+        sm = int(rm.integers(0, 57))
+        shared = np.concatenate([sys_m, subj[sm]])
+        path, qq = snapshot(rm, shared, qm, 2)
+        paths.append(path); q.append(qq); p.append(len(shared) + qm); d.append(2)
+    order = np.random.default_rng([seed, 9]).permutation(len(paths))   # arrival order is not tree order
+    w = _pack(f"c4_grid_t{t:.1f}_s0.5", seed, [paths[i] for i in order], np.asarray(q)[order],
+              np.asarray(p)[order], np.asarray(d)[order], dict(LLAMA8B), "bf16", 64)
+    w.meta.update(counts=(nb, nv, nm), t=t)
+    return w
 
 
 def concat(workloads: List[Workload], name: str) -> Workload:
@@ -244,6 +269,8 @@ def by_name(name: str) -> Workload:
         "c1c_bf16": lambda: c1_tiny("c", "bf16"), "c1d_bf16": lambda: c1_tiny("d", "bf16"),
         "c2": c2_mmlu_decode, "c3": c3_burst_openvid, "c4": c4_grid, "c5": c5_70b_32k,
     }
+    for t in C4_T:
+        table[f"c4_t{t:.1f}"] = (lambda t_=t: c4_grid(t=t_))
     return table[name]()
 
 

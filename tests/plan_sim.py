@@ -88,7 +88,7 @@ def simulate(w, tree):
     T = len(gid)
     Q = np.zeros((T, Hq, D))
     for i in range(T):
-        Q[i] = V.q_values(int(gid[i]), np.array([tt[i]]), w.seed, Hq, D, w.scale_q)[0]
+        Q[i] = V.q_values(int(gid[i]), np.array([tt[i]]), w.seed, Hq, D, w.scale_q, w.head0)[0]
     nprow = tree.plan_info()["n_partial_rows"]
     part_o = np.full((nprow, Hq, D), np.nan)
     part_l = np.full((nprow, Hq), np.nan)
@@ -105,8 +105,8 @@ def simulate(w, tree):
                 page, roff, pos0, cnt = (int(x) for x in P["entries"][e])
                 pi = page_index[page]
                 h = phash[pi * ps + roff: pi * ps + roff + cnt]
-                K.append(V.kv_values(h, w.seed, 0, Hkv, D)[:, kvh])
-                Vv.append(V.kv_values(h, w.seed, 1, Hkv, D)[:, kvh])
+                K.append(V.kv_values(h, w.seed, 0, Hkv, D, w.kv_head0)[:, kvh])
+                Vv.append(V.kv_values(h, w.seed, 1, Hkv, D, w.kv_head0)[:, kvh])
                 kpos.extend(range(pos0, pos0 + cnt))
             K = np.concatenate(K)[:, None, :]
             Vv = np.concatenate(Vv)[:, None, :]

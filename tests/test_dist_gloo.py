@@ -1,10 +1,12 @@
-"""Multi-process (gloo, world size 2) coverage of the data-parallel plumbing:
-every rank builds the global tree through the C ABI, blend_shard assigns whole
-subtrees, each rank builds its shard plan and executes it (CPU plan interpreter
-standing in for the GPU), outputs are all-gathered and re-ordered by req_shard,
-and the assembled result matches the oracle; timings are all-reduced with MAX."""
+"""Multi-process (gloo, world size 2) coverage of the multi-GPU plumbing that bench.py
+runs over NCCL: harness/dp.py's shard_batch (global tree through the C ABI, blend_shard,
+the rank's subtree shard), gather_rows (all-gather of out AND lse, re-assembly in global
+request order by req_shard) and, for head parallelism, tp_heads / gather_heads.  Each
+rank executes its own plan with the CPU plan interpreter (tests/plan_sim.py) standing in
+for the GPU; rank 0 checks the assembled result against the fp64 oracle."""
 import os
 import socket
+from dataclasses import replace
 
 import numpy as np
 import pytest
@@ -23,66 +25,66 @@ def _free_port():
     return port
 
 
-def _worker(rank, port, name, resq):
+def _workload(name):
+    from synth import workloads as W
+    from tests.helpers import random_workload
+    if name == "c1d":
+        return W.replicate(lambda seed: W.c1_tiny("d", "f32", seed=seed), WORLD, 1)
+    if name == "c1b_one_batch":
+        return W.c1_tiny("b", "f32")
+    return random_workload(11, n_req=20, hq=4, hkv=2, max_seg=60)
+
+
+def _worker(rank, port, name, mode, resq):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=WORLD)
     try:
-        from harness.run import build_tree, subset
+        from harness.dp import gather_heads, gather_rows, shard_batch, tp_heads
+        from harness.run import build_tree
+        from oracle import attention as A
         from tests.plan_sim import simulate
-        from synth import workloads as W
-        from tests.helpers import random_workload
 
-        if name == "c1d":
-            w = W.replicate(lambda seed: W.c1_tiny("d", "f32", seed=seed), WORLD, 1)
+        gw = _workload(name)
+        if mode == "dp":
+            w, req_shard, _ = shard_batch(gw, WORLD, rank)
         else:
-            w = random_workload(11, n_req=20, hq=4, hkv=2, max_seg=60)
-        tree = build_tree(w)
-        req_shard, _ = tree.shard(WORLD)
-        mine = np.nonzero(req_shard == rank)[0]
-        ws = subset(w, mine)
-        out, lse, written, _ = simulate(ws, build_tree(ws))
+            gw = replace(gw, num_q_heads=4, num_kv_heads=2) if gw.num_kv_heads < 2 else gw
+            hq, hkv, h0, kvh0 = tp_heads(gw, WORLD, rank)
+            w = replace(gw, num_q_heads=hq, num_kv_heads=hkv, head0=h0, kv_head0=kvh0)
+        out, lse, written, _ = simulate(w, build_tree(w))
         assert np.all(written == 1)
-        # gather (padded) outputs over the process group
-        rows = torch.tensor([out.shape[0]])
-        dist.all_reduce(rows, op=dist.ReduceOp.MAX)
-        pad = torch.zeros((int(rows.item()),) + out.shape[1:], dtype=torch.float64)
-        pad[:out.shape[0]] = torch.from_numpy(out)
-        gathered = [torch.zeros_like(pad) for _ in range(WORLD)]
-        dist.all_gather(gathered, pad)
+        o_t, l_t = torch.from_numpy(out), torch.from_numpy(lse)
+        if mode == "dp":
+            of, lf = gather_rows(o_t, l_t, gw, req_shard, WORLD, dist)
+        else:
+            of, lf = gather_heads(o_t, l_t, WORLD, dist)
         t = torch.tensor([float(rank + 1)])
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         if rank == 0:
-            # re-assemble in global request order
-            q = w.q_len.astype(np.int64)
-            qo = np.concatenate([[0], np.cumsum(q)])
-            full = np.zeros((int(q.sum()),) + out.shape[1:])
-            for g in range(WORLD):
-                rs = np.nonzero(req_shard == g)[0]
-                off = 0
-                for r in rs:
-                    full[qo[r]:qo[r + 1]] = gathered[g][off:off + q[r]].numpy()
-                    off += q[r]
-            from oracle import attention as A
-            ref = A.attention_workload(w)
-            err = max(float(np.max(np.abs(full[qo[r]:qo[r + 1]] - ref[r][0]))) for r in range(w.n_req))
-            resq.put((err, float(t.item()), [int((req_shard == g).sum()) for g in range(WORLD)]))
+            ref = A.attention_workload(gw)
+            qo = np.concatenate([[0], np.cumsum(gw.q_len)])
+            err = max(float(np.max(np.abs(of[qo[r]:qo[r + 1]].numpy() - O))) for r, (O, L) in ref.items())
+            lerr = max(float(np.max(np.abs(lf[qo[r]:qo[r + 1]].numpy() - L))) for r, (O, L) in ref.items())
+            counts = [int((req_shard == g).sum()) for g in range(WORLD)] if mode == "dp" else [w.num_q_heads] * 2
+            resq.put((err, lerr, float(t.item()), counts))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name", ["c1d", "random"])
-def test_gloo_shard_gather(name):
+@pytest.mark.parametrize("name,mode", [("c1d", "dp"), ("random", "dp"), ("c1b_one_batch", "dp"),
+                                       ("random", "tp")])
+def test_gloo_multi_rank(name, mode):
     ctx = mp.get_context("spawn")
     q = ctx.SimpleQueue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, port, name, q)) for r in range(WORLD)]
+    procs = [ctx.Process(target=_worker, args=(r, port, name, mode, q)) for r in range(WORLD)]
     for p in procs:
         p.start()
     for p in procs:
         p.join(timeout=300)
         assert p.exitcode == 0
-    err, tmax, counts = q.get()
-    assert err < 1e-10
+    err, lerr, tmax, counts = q.get()
+    assert err < 1e-10 and lerr < 1e-10
     assert tmax == WORLD
     assert all(c > 0 for c in counts)

@@ -112,9 +112,9 @@ def _needle_picks(w, rng, n_pick, late_frac=0.6, want_big=None):
 @pytest.mark.parametrize("seed", range(6))
 def test_random_trees_peaked(seed):
     """Peaked Q (scale 8: bf16-exact k/16 values, score std ~ 2.7) on random forests with
-    long nodes, the three kernel paths and three plan shapes; the counters show both
-    passes ran and the streaming rescale fired (the dense lazy rescale needs a jump of
-    > 2^8 over the running max: test_needles_fire_dense_lazy_rescale forces it)."""
+    long nodes, the three kernel paths and three plan shapes; the counters show that the
+    dense late max-first path, the dense lazy O rescale (a jump of > 2^8 over the running
+    max) and the streaming rescale all fired (B200 run: 110..2100 lazy rescales per seed)."""
     hq, hkv = [(8, 2), (32, 8), (16, 4)][seed % 3]
     w = random_workload(300 + seed, hq=hq, hkv=hkv, d=128 if seed % 2 == 0 else 64, kv_dtype="bf16",
                         page_size=[64, 16, 32][seed % 3], max_seg=400, n_req=int(14 + 2 * seed), scale_q=8.0)
@@ -129,7 +129,8 @@ def test_random_trees_peaked(seed):
                 for k in tot:
                     tot[k] += st[k]
     assert tot["dense_blocks"] > 0 and tot["stream_stages"] > 0, tot
-    assert tot["stream_rescale"] > 0, tot
+    assert tot["dense_slow_late"] > 0 and tot["dense_rescale"] > 0, tot
+    assert tot["stream_rescale"] > 0 and tot["tail_zeroed"] > 0, tot
     print("path counters", tot)
 
 

@@ -390,3 +390,29 @@ def test_keys_match_distinct_prompt_bruteforce(seed):
         S = [r for r in range(w.n_req) if len(w.path(r)) >= s + ln and np.array_equal(w.path(r)[:s + ln], full)]
         assert len(S) == int(v["node_nreq"][i])
         assert (v["cu"][i], v["mu"][i]) == _bruteforce_key(w, S, Pm, HL4), i
+
+
+@pytest.mark.parametrize("p,d,n", [(64, 16, 40), (728, 256, 900), (228, 16384, 300), (1100, 2, 1101)])
+def test_request_key_is_single_request_tree_key(p, d, n):
+    w = from_paths([list(range(1000, 1000 + n))], p=[p], d=[d])
+    v = T.build(w)
+    assert T.request_key(p, d, 8_030_261_248, 4096, 32) == (v["cu"][0], v["mu"][0])
+    # P:379 worked example with A100 constants: BurstGPT-like 3.73, OpenVid-like 0.096
+    assert abs(T.density(*T.request_key(728, 256, 8_030_261_248, 4096, 32), A100_TF, A100_BW, 131072) / 3.73 - 1) < 0.02
+
+
+def test_root_key_adds_disjoint_subtrees_and_sharing_ratio():
+    # two disjoint trees: the root key is the sum of the top-level keys; a batch of identical
+    # prompts shares (N-1)/N of its prompt GEMM tokens, here with d = 0
+    rng = np.random.default_rng(3)
+    a, b = list(rng.integers(1000, 32000, 50)), list(rng.integers(1000, 32000, 70))
+    w = from_paths([a + [1], a + [2], b + [3]], p=[51, 51, 71], d=[5, 6, 7])
+    v = T.build(w)
+    tops = [i for i in range(v["n_nodes"]) if v["node_parent"][i] < 0]
+    assert len(tops) == 2
+    assert T.root_key(v) == (sum(v["cu"][i] for i in tops), sum(v["mu"][i] for i in tops))
+    w2 = from_paths([a] * 4, p=[50] * 4, d=[0] * 4)
+    v2 = T.build(w2)
+    Pm, HL4 = 8_030_261_248, 4 * 4096 * 32
+    s = T.sharing_ratio(w2, v2)
+    assert s == pytest.approx(1 - (2 * Pm * 50 + HL4 * 4 * 2500) / (4 * (2 * Pm * 50 + HL4 * 2500)), rel=1e-12)
