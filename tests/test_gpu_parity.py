@@ -249,51 +249,74 @@ def test_group_sizes_bf16(hq, hkv, d, ps):
         _cmp(w, db)
 
 
-@pytest.mark.parametrize("G", [2, 4])
-def test_sharded_equals_single_gpu(G):
-    """§8(e) invariant "G-GPU == 1-GPU" on one device: the bench's N-GPU recipe (N
-    independent C2 copies), sharded by blend_shard into G subtree shards, each shard
-    planned and run on its own; re-assembled in global request order the outputs equal
-    the unsharded run's within the bf16 tolerance (different plans, so not bitwise) and
-    the oracle on a sample of requests."""
-    from harness.run import build_tree, subset
-    gw = W.replicate(lambda seed: W.c2_mmlu_decode(n_req=48, seed=seed), G, 2)
+@pytest.mark.parametrize("name,G", [("c2", 2), ("c2", 4), ("c5", 8), ("c2x2", 2)])
+def test_sharded_equals_single_gpu(name, G):
+    """§8(e) invariant "G-GPU == 1-GPU" on one device, through the bench's own DP code
+    (harness/dp.py): ONE global batch (c2x2: two independent C2 copies) is sharded by
+    blend_shard into G subtree shards, each shard planned, filled and run on its own, and
+    the rows re-assembled in global request order by row_index (what gather_rows does after
+    the all-gather) equal the unsharded run within the bf16 tolerance (different plans,
+    so not bitwise) and match the oracle on sampled requests."""
+    from harness.dp import row_index, shard_batch
+    if name == "c2x2":
+        gw = W.replicate(lambda seed: W.c2_mmlu_decode(n_req=48, seed=seed), 2, 2)
+    else:
+        gw = W.by_name(name)
     dbg = device_batch(gw)
     dbg.run()
     torch.cuda.synchronize()
-    full = dbg.out.float().cpu().numpy()
-    req_shard, _ = build_tree(gw).shard(G)
-    qo = np.concatenate([[0], np.cumsum(gw.q_len)])
-    seen = np.zeros(gw.n_req, dtype=bool)
+    full_o, full_l = dbg.out.float().cpu(), dbg.lse.cpu()
+    del dbg
+    got_o = torch.full_like(full_o, float("nan"))
+    got_l = torch.full_like(full_l, float("nan"))
     for g in range(G):
-        mine = np.nonzero(req_shard == g)[0]
-        assert len(mine) > 0
-        ws = subset(gw, mine)
+        ws, req_shard, _ = shard_batch(gw, G, g)
+        assert ws.n_req > 0
+        if name == "c5" and G == 8:   # P:246 / SURVEY c-5: subtree snapping -> 2 whole documents per GPU
+            docs = {int(ws.path(r)[256]) for r in range(ws.n_req)}
+            assert len(docs) == 2 and ws.n_req == 128
         db = device_batch(ws)
         db.run()
         torch.cuda.synchronize()
-        o = db.out.float().cpu().numpy()
-        qs = np.concatenate([[0], np.cumsum(ws.q_len)])
-        for i, r in enumerate(mine):
-            a, b = full[qo[r]:qo[r + 1]], o[qs[i]:qs[i + 1]]
-            assert np.max(np.abs(a - b)) <= 2e-2, (g, int(r))
-            seen[r] = True
-        _cmp(ws, db, requests=list(range(0, ws.n_req, max(1, ws.n_req // 6))))
-    assert seen.all(), "every request in exactly one shard"
+        ix = torch.from_numpy(row_index(gw, req_shard, G)[g])
+        got_o[ix] = db.out.float().cpu()
+        got_l[ix] = db.lse.cpu()
+        _cmp(ws, db, requests=list(range(0, ws.n_req, max(1, ws.n_req // 4))))
+        del db
+    assert not torch.isnan(got_l).any(), "every row in exactly one shard"
+    assert (got_o - full_o).abs().max().item() <= 2e-2
+    assert (got_l - full_l).abs().max().item() <= 1e-3
 
 
-def test_tp_head_slice():
-    """NEXT-4 head-parallel replicas: a rank's slice of the heads (Hq/N query heads over
-    Hkv/N kv heads, whole batch) is an ordinary plan; C5-shaped groups (g = 8) sliced to
-    one kv head match the oracle."""
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_tp_slices_concat_to_full(n):
+    """NEXT-4 head parallelism on the full C5 batch (70B shapes, 64/8 heads): rank k
+    of n runs kv heads [8k/n, 8(k+1)/n) with global head indices in the synthetic values;
+    the n slices concatenated along the head axis equal the full-head run bitwise (same
+    split-KV plan: split sizes pinned) and match the oracle on sampled requests."""
     from dataclasses import replace
-    w0 = W.c2_mmlu_decode(n_req=40)
-    for hq, hkv in ((8, 2), (4, 1)):
-        w = replace(w0, num_q_heads=hq, num_kv_heads=hkv, name=f"{w0.name}_tp_{hq}_{hkv}")
-        db = device_batch(w)
+    from harness.dp import tp_heads
+    gw = W.c5_70b_32k()
+    kw = dict(split_tokens=4096, dense_split=2)
+    full = device_batch(gw, tree_kw=kw)
+    full.run()
+    torch.cuda.synchronize()
+    fo, fl = full.out.cpu(), full.lse.cpu()
+    del full
+    outs, lses = [], []
+    for k in range(n):
+        hq, hkv, h0, kvh0 = tp_heads(gw, n, k)
+        w = replace(gw, num_q_heads=hq, num_kv_heads=hkv, head0=h0, kv_head0=kvh0)
+        db = device_batch(w, tree_kw=kw)
         db.run()
         torch.cuda.synchronize()
-        _cmp(w, db)
+        outs.append(db.out.cpu())
+        lses.append(db.lse.cpu())
+        if k == n - 1:
+            _cmp(w, db, requests=[0, 63, 500, 1023])      # the slice against the oracle's heads
+        del db
+    assert torch.equal(torch.cat(outs, dim=1), fo)
+    assert torch.equal(torch.cat(lses, dim=1), fl)
 
 
 @pytest.mark.parametrize("seed", range(8, 16))
