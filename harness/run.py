@@ -16,14 +16,14 @@ from synth import values as V
 
 
 def build_tree(w, rows_min=128, min_sep_len=128, force_class=0, split_tokens=0, num_sms=148,
-               free_pages=None, dense_split=0):
+               free_pages=None, dense_split=0, split_waste=0):
     fp = w.free_pages if free_pages is None else free_pages
     return B.build(w.tokens, w.tok_off, w.q_len, w.prompt_len, w.out_len,
                    num_q_heads=w.num_q_heads, num_kv_heads=w.num_kv_heads, head_dim=w.head_dim,
                    kv_dtype=w.kv_dtype, model_params=w.model_params, hidden=w.hidden, layers=w.layers,
                    page_size=w.page_size, free_pages=fp, global_id=w.global_id, rows_min=rows_min,
                    min_sep_len=min_sep_len, force_class=force_class, split_tokens=split_tokens,
-                   num_sms=num_sms, dense_split=dense_split)
+                   num_sms=num_sms, dense_split=dense_split, split_waste=split_waste)
 
 
 def page_slot_hashes(w, view):

@@ -87,6 +87,11 @@ typedef struct {
   int32_t split_tokens;        /* streaming split-KV chunk in tokens, 0 = auto (plan only)       */
   int32_t num_sms;             /* SM count the plan is sized for, 0 = 148 (B200)                */
   int32_t dense_split;         /* split-KV factor of dense items, 0 = auto (plan only)            */
+  int32_t split_waste;         /* Alg. 2 conditional node splitting threshold t in
+                                  tokens: an outlier subtree (density on the other side of the
+                                  root density than its siblings') is relocated to the top level,
+                                  duplicating its shared prefix, iff that prefix is <= t tokens.
+                                  0 = off                                                        */
 } blend_build_args;
 
 typedef struct blend_tree blend_tree;   /* opaque, host-owned */
@@ -114,6 +119,7 @@ typedef struct {
   const uint8_t* req_class;        /* [R] 1 = BIG (q_len*g >= rows_min), 0 = SMALL          */
   const int32_t* req_dfs_rank;     /* [R] position of the request in the DFS order          */
   const int64_t* req_global_id;    /* [R] global request index                              */
+  const int32_t* req_group;        /* [R] Alg. 2 relocation group (0 = not relocated)        */
 } blend_tree_view;
 
 /* Build the descriptors for one batch.  Errors: EINVAL (dims, flags, NULLs,
@@ -144,6 +150,55 @@ int blend_tree_dump(const blend_tree* tree, char* buf, size_t cap, size_t* need)
 int blend_shard(const blend_tree* tree, int32_t n_shards, int64_t kappa,
                 const int32_t* const* shard_free_pages, const int64_t* n_shard_free,
                 int32_t* req_shard, blend_tree** shards);
+
+/* ------------------------------------------------------------------------ */
+/* Dual-scanner batch former (host only), NEXT-2: PAPER §4.4 P:354-380.        */
+/* ------------------------------------------------------------------------ */
+/* The tree is a whole offline workload: each request's path is its full PROMPT
+ * (prompt_len = path length) and out_len its output length d.  The former walks the
+ * density-sorted tree's scanner units (a node whose children are all single-request
+ * leaves is one merged unit, P:7) from both ends with two cursors, splits the KV memory
+ * M into M_L + M_R = M with M_L rho(R_L) + M_R rho(R_R) = M rho(rt) whenever a cursor
+ * moves (exact integer arithmetic, floor), admits requests per side while
+ * their footprint p + d fits (continuous batching), reuses the prompt prefix an
+ * active request already materialised (runtime prefix cache), and emits one blended
+ * batch per step: chunked prefill (<= chunk tokens per request, <= step_budget per step)
+ * then d decode steps.  Deterministic; readings in DESIGN.md §3 #25-#31. */
+enum { BLEND_SCHED_DUAL = 0, BLEND_SCHED_DFS = 1 };
+
+typedef struct {
+  int64_t mem_tokens;     /* M: KV memory in tokens (all layers), > 0                      */
+  int32_t chunk;          /* chunked-prefill tokens per request per step, 0 = 512           */
+  int32_t step_budget;    /* prefill tokens per step, 0 = 8192                              */
+  int32_t policy;         /* BLEND_SCHED_DUAL, or BLEND_SCHED_DFS: the tree's DFS order on one
+                             side with all of M (the sharing reference)              */
+  int64_t max_steps;      /* stop after this many steps, 0 = run to completion              */
+} blend_sched_args;
+
+typedef struct blend_schedule blend_schedule;   /* opaque, host-owned */
+
+/* Read-only arrays owned by the schedule (valid until blend_schedule_free). */
+typedef struct {
+  int64_t n_steps, n_entries;
+  int32_t n_req, n_admitted;
+  const int64_t* step_off;     /* [n_steps+1] CSR of the steps' batch entries            */
+  const int32_t* req;          /* [n_entries] tree request index                         */
+  const int32_t* n_cached;     /* [n_entries] the request's cached path length after the step
+                                  (prompt[:n] while prefilling; prompt + n - p generated
+                                  tokens while decoding): the step batch's path length   */
+  const int32_t* q;            /* [n_entries] the step's query tokens (last q of the path) */
+  const int32_t* order;        /* [n_admitted] requests in admission order               */
+  const uint8_t* side;         /* [n_req] 0 = left (compute-intensive), 1 = right cursor  */
+  const int64_t* m_left;       /* [n_steps] M_L in force during the step                 */
+  int64_t cached_prompt_tokens;   /* prompt tokens reused from the runtime cache           */
+  int64_t optimal_cached_tokens;  /* sum p - distinct prompt tokens (P:480's optimum)       */
+} blend_schedule_view;
+
+/* EINVAL (NULLs, mem_tokens <= 0, negative chunk / budget / max_steps, bad policy),
+ * ENOMEM.  Reentrant. */
+int blend_schedule_build(const blend_tree* tree, const blend_sched_args* args, blend_schedule** out);
+int blend_schedule_get_view(const blend_schedule* sched, blend_schedule_view* view);
+void blend_schedule_free(blend_schedule* sched);
 
 /* ------------------------------------------------------------------------ */
 /* Work plan + attention (device).                                            */

@@ -84,7 +84,9 @@ def _validate(w, rows_min, min_sep_len, force_class, n_free):
         raise BlendError(EMALFORMED, "negative token id")
 
 
-def _build_trie(w):
+def _build_trie(w, group=None):
+    """Radix insertion.  group[r] (Alg. 2 relocation group, 0 = none) separates requests
+    at the root: relocated requests never share a node with other groups."""
     root = _Node(0, 0, -1)
     for r in range(w.n_req):
         P = w.path(r)
@@ -92,11 +94,12 @@ def _build_trie(w):
         node, pos = root, 0
         while True:
             tok = int(P[pos])
-            child = node.children.get(tok)
+            key = (int(group[r]) if group is not None else 0, tok) if node is root else tok
+            child = node.children.get(key)
             if child is None:
                 leaf = _Node(pos, n - pos, r, parent=node)
                 leaf.ends.append(r)
-                node.children[tok] = leaf
+                node.children[key] = leaf
                 break
             seg = w.path(child.ref)[child.start:child.start + child.length]
             L = min(child.length, n - pos)
@@ -104,7 +107,7 @@ def _build_trie(w):
             k = int(neq[0]) if neq.size else L
             if k < child.length:                       # split child at k
                 upper = _Node(child.start, k, child.ref, parent=node)
-                node.children[tok] = upper
+                node.children[key] = upper
                 child.start += k
                 child.length -= k
                 child.parent = upper
@@ -126,12 +129,76 @@ def _all_nodes(root):
     return out
 
 
+def relocation_groups(w, view, split_waste: int):
+    """Alg. 2 conditional node splitting (its body is missing, P:353 -> the
+    reading in DESIGN.md §3 #24): walk the density-sorted tree top-down; a child c of a
+    node with >= 2 children is an OUTLIER when its density lies strictly on the other side
+    of the root density rho(rt) than the strict majority of its siblings' requests (each
+    sibling subtree counts its |A| requests on the side of its own density; the dual
+    scanner only needs each request on the correct side).  Relocating c
+    duplicates the prefix it shares with its siblings, start(c) tokens ("potential
+    recomputation waste"); it happens iff start(c) <= split_waste (the threshold t).  A
+    relocated subtree is not searched further.  Returns group[r] (0 = stays, k >= 1 =
+    the k-th relocated subtree in preorder)."""
+    n = view["n_nodes"]
+    cu_rt, mu_rt = root_key(view)
+    kids = [[] for _ in range(n)]
+    for i in range(n):
+        par = int(view["node_parent"][i])
+        if par >= 0:
+            kids[par].append(i)
+
+    def side(cu, mu):          # sign(rho - rho_rt) with rho = cu / mu, MU = 0 -> +inf
+        if mu == 0:
+            return 1 if cu > 0 or mu_rt > 0 else 0
+        a, b = cu * mu_rt, cu_rt * mu
+        return (a > b) - (a < b)
+
+    group = np.zeros(w.n_req, dtype=np.int32)
+    relocated = []
+
+    def subtree_reqs(x):
+        out, st = [], [x]
+        while st:
+            y = st.pop()
+            out.extend(view["node_ends"][y])
+            st.extend(kids[y])
+        return out
+
+    stack = [i for i in range(n) if int(view["node_parent"][i]) < 0][::-1]
+    while stack:
+        x = stack.pop()
+        ch = kids[x]
+        moved = set()
+        if len(ch) >= 2:
+            sides = {c: side(view["cu"][c], view["mu"][c]) for c in ch}
+            for c in ch:
+                up = sum(int(view["node_nreq"][o]) for o in ch if o != c and sides[o] > 0)
+                down = sum(int(view["node_nreq"][o]) for o in ch if o != c and sides[o] < 0)
+                ss = (up > down) - (up < down)
+                sc = sides[c]
+                if sc != 0 and ss != 0 and sc != ss and int(view["node_start"][c]) <= split_waste:
+                    moved.add(c)
+                    relocated.append(c)
+        for c in reversed(ch):
+            if c not in moved:
+                stack.append(c)
+    for k, c in enumerate(sorted(relocated), start=1):     # preorder ids = sorted node ids
+        for r in subtree_reqs(c):
+            group[r] = k
+    return group
+
+
 def build(w, rows_min: int = 128, min_sep_len: int = 128, force_class: int = 0,
-          free_pages=None) -> dict:
-    """Return the descriptor view (dict of numpy arrays + ints) for workload w."""
+          free_pages=None, split_waste: int = 0) -> dict:
+    """Return the descriptor view (dict of numpy arrays + ints) for workload w.
+    split_waste > 0 applies Alg. 2 (relocation_groups) to the sorted tree and rebuilds."""
     free = w.free_pages if free_pages is None else free_pages
     _validate(w, rows_min, min_sep_len, force_class, None if free is None else len(free))
-    root = _build_trie(w)
+    group = None
+    if split_waste > 0:
+        group = relocation_groups(w, build(w, rows_min, min_sep_len, force_class, free_pages), split_waste)
+    root = _build_trie(w, group)
     nodes = _all_nodes(root)
     n_path = np.diff(w.tok_off).astype(object)
     p = [int(x) for x in w.prompt_len]
@@ -272,6 +339,7 @@ def build(w, rows_min: int = 128, min_sep_len: int = 128, force_class: int = 0,
         req_dfs_rank=rank,
         req_global_id=(np.asarray(w.global_id, dtype=np.int64) if w.global_id is not None
                        else np.arange(R, dtype=np.int64)),
+        req_group=(group if group is not None else np.zeros(R, dtype=np.int32)),
         # python-int keys for readability in tests
         cu=[CU[id(x)] for x in order], mu=[MU[id(x)] for x in order],
         dfs_order=np.array(dfs_req, dtype=np.int32),

@@ -45,7 +45,7 @@ class BuildArgs(C.Structure):
                 ("layers", C.c_int32), ("page_size", C.c_int32), ("free_pages", C.c_void_p),
                 ("n_free_pages", C.c_int64), ("rows_min", C.c_int32), ("min_sep_len", C.c_int32),
                 ("force_class", C.c_int32), ("split_tokens", C.c_int32), ("num_sms", C.c_int32),
-                ("dense_split", C.c_int32)]
+                ("dense_split", C.c_int32), ("split_waste", C.c_int32)]
 
 
 class TreeView(C.Structure):
@@ -53,7 +53,7 @@ class TreeView(C.Structure):
         (n, C.c_void_p) for n in (
             "node_parent", "node_start", "node_len", "node_page_off", "node_class", "node_key_cu",
             "node_key_mu", "node_first_req", "node_nreq", "page_table", "req_path_off",
-            "req_path_nodes", "req_q_off", "req_class", "req_dfs_rank", "req_global_id")]
+            "req_path_nodes", "req_q_off", "req_class", "req_dfs_rank", "req_global_id", "req_group")]
 
 
 class PlanInfo(C.Structure):
@@ -78,6 +78,20 @@ class AttnArgs(C.Structure):
                 ("flags", C.c_int32), ("events", C.c_void_p * 4)]
 
 
+class SchedArgs(C.Structure):
+    _fields_ = [("mem_tokens", C.c_int64), ("chunk", C.c_int32), ("step_budget", C.c_int32),
+                ("policy", C.c_int32), ("max_steps", C.c_int64)]
+
+
+class SchedView(C.Structure):
+    _fields_ = [("n_steps", C.c_int64), ("n_entries", C.c_int64), ("n_req", C.c_int32),
+                ("n_admitted", C.c_int32)] + [(n, C.c_void_p) for n in (
+                    "step_off", "req", "n_cached", "q", "order", "side", "m_left")] + [
+                ("cached_prompt_tokens", C.c_int64), ("optimal_cached_tokens", C.c_int64)]
+
+
+SCHED_DUAL, SCHED_DFS = 0, 1
+
 _lib = None
 
 EXPORTS = {
@@ -99,6 +113,9 @@ EXPORTS = {
     "blend_fill_q": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                C.c_int64, C.c_uint64, C.c_float, C.c_void_p]),
     "blend_l2_flush": (C.c_int, [C.c_void_p, C.c_size_t, C.c_void_p]),
+    "blend_schedule_build": (C.c_int, [C.c_void_p, C.POINTER(SchedArgs), C.POINTER(C.c_void_p)]),
+    "blend_schedule_get_view": (C.c_int, [C.c_void_p, C.POINTER(SchedView)]),
+    "blend_schedule_free": (None, [C.c_void_p]),
 }
 
 
@@ -185,6 +202,7 @@ class Tree:
             req_class=get(v.req_class, C.c_uint8, R, np.uint8),
             req_dfs_rank=get(v.req_dfs_rank, C.c_int32, R, np.int32),
             req_global_id=get(v.req_global_id, C.c_int64, R, np.int64),
+            req_group=get(v.req_group, C.c_int32, R, np.int32),
         )
 
     def dump(self) -> str:
@@ -229,6 +247,29 @@ class Tree:
         _check(lib().blend_tree_get_view(self._h, C.byref(v)))
         return v.n_req
 
+    def schedule(self, mem_tokens: int, chunk: int = 512, step_budget: int = 8192, policy: int = 0,
+                 max_steps: int = 0) -> dict:
+        """blend_schedule_build on this (whole-workload) tree: the dual-scanner batch stream."""
+        a = SchedArgs(mem_tokens, chunk, step_budget, policy, max_steps)
+        h = C.c_void_p()
+        _check(lib().blend_schedule_build(self._h, C.byref(a), C.byref(h)))
+        try:
+            v = SchedView()
+            _check(lib().blend_schedule_get_view(h, C.byref(v)))
+
+            def get(ptr, ctype, n, dt):
+                if n == 0:
+                    return np.zeros(0, dtype=dt)
+                return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(ctype)), (n,)).astype(dt, copy=True)
+            E, S = v.n_entries, v.n_steps
+            return dict(n_steps=S, step_off=get(v.step_off, C.c_int64, S + 1, np.int64),
+                        req=get(v.req, C.c_int32, E, np.int32), n_cached=get(v.n_cached, C.c_int32, E, np.int32),
+                        q=get(v.q, C.c_int32, E, np.int32), order=get(v.order, C.c_int32, v.n_admitted, np.int32),
+                        side=get(v.side, C.c_uint8, v.n_req, np.uint8), m_left=get(v.m_left, C.c_int64, S, np.int64),
+                        cached_prompt_tokens=v.cached_prompt_tokens, optimal_cached_tokens=v.optimal_cached_tokens)
+        finally:
+            lib().blend_schedule_free(h)
+
     def upload_plan(self, dev_buf, stream=None) -> Plan:
         """Copy the plan into dev_buf (a CUDA tensor of >= plan_bytes bytes)."""
         plan = Plan()
@@ -242,7 +283,7 @@ class Tree:
 def build(tokens, tok_off, q_len, prompt_len, out_len, *, num_q_heads, num_kv_heads, head_dim,
           kv_dtype="bf16", model_params=8_030_261_248, hidden=4096, layers=32, page_size=64,
           free_pages=None, global_id=None, rows_min=128, min_sep_len=128, force_class=0,
-          split_tokens=0, num_sms=148, dense_split=0) -> Tree:
+          split_tokens=0, num_sms=148, dense_split=0, split_waste=0) -> Tree:
     """blend_tree_build on host arrays (numpy-convertible).  Array lengths are checked
     here (the C side trusts n_req = len(q_len)): ValueError on a mismatch."""
     keep = []
@@ -271,6 +312,7 @@ def build(tokens, tok_off, q_len, prompt_len, out_len, *, num_q_heads, num_kv_he
         a.n_free_pages = len(fp)
     a.rows_min, a.min_sep_len, a.force_class = rows_min, min_sep_len, force_class
     a.split_tokens, a.num_sms, a.dense_split = split_tokens, num_sms, dense_split
+    a.split_waste = split_waste
     h = C.c_void_p()
     _check(lib().blend_tree_build(C.byref(a), C.byref(h)))
     return Tree(h.value)

@@ -23,9 +23,7 @@
 
 #include "blend.h"
 #include "internal.h"
-
-using u128 = unsigned __int128;
-using i128 = __int128;
+#include "tree.h"
 
 namespace {
 
@@ -72,39 +70,6 @@ bool gt256(U256 a, U256 b) { return a.hi != b.hi ? a.hi > b.hi : a.lo > b.lo; }
 
 }  // namespace
 
-struct blend_tree {
-  // ---- owned inputs
-  blend_build_args args{};
-  std::vector<int64_t> tok_off;
-  std::vector<int32_t> tokens, q_len, prompt_len, out_len, free_pages;
-  std::vector<int64_t> global_id;
-  bool has_free = false;
-  int32_t rows_min = 128, min_sep_len = 128, force_class = 0;
-  // ---- descriptors
-  int32_t n_req = 0, n_nodes = 0;
-  std::vector<int32_t> node_parent, node_start, node_len, node_first_req, node_nreq;
-  std::vector<int64_t> node_page_off;
-  std::vector<uint8_t> node_class;
-  std::vector<uint64_t> node_key_cu, node_key_mu;
-  std::vector<u128> cu, mu;
-  std::vector<int32_t> node_end_off, node_end_req;   // requests ending at each node (ascending)
-  std::vector<int32_t> page_table;
-  std::vector<int64_t> req_path_off;
-  std::vector<int32_t> req_path_nodes;
-  std::vector<int64_t> req_q_off;
-  std::vector<uint8_t> req_class;
-  std::vector<int32_t> req_dfs_rank, dfs_order;
-  // ---- plan (host image of the device plan buffer)
-  std::vector<uint8_t> plan_blob;
-  int64_t sec_off[16] = {0}, sec_count[16] = {0};
-  blend_plan_info info{};
-  size_t workspace_bytes = 0;
-  int64_t n_partial_rows = 0;
-  int64_t stream_entries = 0;   // sum over stream units of their entry counts (launch heuristic)
-  int32_t dense_ctas = 0;       // dense-pass grid cap (0: one CTA per SM), set by the planner
-  int32_t merge_nsrc = 0;       // > 0: every merge list has this many sources
-  int32_t max_page = -1;        // largest physical page id in page_table (-1: no pages)
-};
 
 namespace {
 
@@ -126,7 +91,7 @@ int validate(const blend_build_args* a) {
     return fail(BLEND_EINVAL, "page_size must be a power of two in [16,128]");
   if (a->kv_dtype != BLEND_BF16 && a->kv_dtype != BLEND_F32) return fail(BLEND_EINVAL, "kv_dtype");
   if (a->rows_min < 0 || a->min_sep_len < -1 || a->force_class < 0 || a->force_class > 2 ||
-      a->split_tokens < 0 || a->num_sms < 0 || a->dense_split < 0)
+      a->split_tokens < 0 || a->num_sms < 0 || a->dense_split < 0 || a->split_waste < 0)
     return fail(BLEND_EINVAL, "rows_min/min_sep_len/force_class/split_tokens/num_sms");
   if (a->n_req < 1) return fail(BLEND_EINVAL, "n_req must be >= 1");
   if (!a->tok_off || !a->tokens || !a->q_len || !a->prompt_len || !a->out_len)
@@ -148,6 +113,7 @@ int validate(const blend_build_args* a) {
 
 int build_descriptors(blend_tree* t);
 int build_plan(blend_tree* t);
+bool relocation_groups(blend_tree* t, int64_t split_waste);
 
 int build_impl(const blend_build_args* a, blend_tree** out) {
   int st = validate(a);
@@ -183,7 +149,11 @@ int build_impl(const blend_build_args* a, blend_tree** out) {
     t->rows_min = a->rows_min == 0 ? 128 : a->rows_min;
     t->min_sep_len = a->min_sep_len < 0 ? 128 : a->min_sep_len;
     t->force_class = a->force_class;
+    t->req_group.assign(R, 0);
     st = build_descriptors(t);
+    // Alg. 2 (conditional node splitting): relocate outlier subtrees of the sorted tree
+    // and rebuild with each relocated subtree in its own root-level group
+    if (!st && a->split_waste > 0 && relocation_groups(t, a->split_waste)) st = build_descriptors(t);
     if (!st) st = build_plan(t);
   } catch (const std::bad_alloc&) {
     st = fail(BLEND_ENOMEM, "out of host memory");
@@ -212,7 +182,9 @@ int build_descriptors(blend_tree* t) {
   for (int32_t r = 0; r < R; ++r) {
     const int32_t* P = tok + off[r];
     const int32_t n = int32_t(off[r + 1] - off[r]);
-    int32_t node = -1, pos = 0;
+    // the root of relocation group g is the pseudo-parent -1 - g: relocated requests
+    // never share a node with another group (Alg. 2 duplicates their prefix)
+    int32_t node = -1 - t->req_group[r], pos = 0;
     for (;;) {
       auto it = child.find(ckey(node, P[pos]));
       if (it == child.end()) {
@@ -402,6 +374,7 @@ int build_descriptors(blend_tree* t) {
   // ---- 6. request paths, classes
   const int32_t g = a.num_q_heads / a.num_kv_heads;
   t->req_path_off.assign(R + 1, 0);
+  t->req_path_nodes.clear();
   std::vector<int32_t> chain;
   for (int32_t r = 0; r < R; ++r) {
     chain.clear();
@@ -428,6 +401,69 @@ int build_descriptors(blend_tree* t) {
     if ((int64_t)g * small_q[i] >= t->rows_min && t->node_len[i] >= t->min_sep_len) t->node_class[i] = 1;
   }
   return BLEND_OK;
+}
+
+// Alg. 2, conditional node splitting (the algorithm body is missing, P:353,
+// DESIGN.md reading #24): a child c of a node with >= 2 children is an outlier when its
+// density lies strictly on the other side of the root density rho(rt) than the strict
+// majority of its siblings' requests (a sibling subtree's |A| requests count on the side
+// of its own density); it is relocated (its prefix duplicated) iff the prefix it shares,
+// start(c) tokens, is <= split_waste.  Relocated subtrees are not searched further.
+// Sets req_group (k >= 1: the k-th relocated node in preorder); false if none moved.
+bool relocation_groups(blend_tree* t, int64_t split_waste) {
+  const int32_t NN = t->n_nodes, R = t->n_req;
+  u128 cu_rt = 0, mu_rt = 0;
+  std::vector<std::vector<int32_t>> kids(NN);
+  for (int32_t i = 0; i < NN; ++i) {
+    if (t->node_parent[i] < 0) {
+      cu_rt += t->cu[i];
+      mu_rt += t->mu[i];
+    } else {
+      kids[t->node_parent[i]].push_back(i);
+    }
+  }
+  auto side = [&](u128 cu, u128 mu) -> int {   // sign(cu / mu - cu_rt / mu_rt), mu = 0 -> +inf
+    if (mu == 0) return (cu > 0 || mu_rt > 0) ? 1 : 0;
+    const U256 a = mul_full(cu, mu_rt), b = mul_full(cu_rt, mu);
+    return gt256(a, b) ? 1 : (gt256(b, a) ? -1 : 0);
+  };
+  std::vector<char> moved(NN, 0), blocked(NN, 0);
+  bool any = false;
+  for (int32_t x = 0; x < NN; ++x) {   // preorder: a parent precedes its children
+    if (t->node_parent[x] >= 0 && (blocked[t->node_parent[x]] || moved[t->node_parent[x]])) blocked[x] = 1;
+    if (blocked[x] || moved[x] || kids[x].size() < 2) continue;
+    int64_t up = 0, down = 0;   // requests of the children on each side of rho(rt)
+    std::vector<int> sd(kids[x].size());
+    for (size_t i = 0; i < kids[x].size(); ++i) {
+      const int32_t c = kids[x][i];
+      sd[i] = side(t->cu[c], t->mu[c]);
+      if (sd[i] > 0) up += t->node_nreq[c];
+      if (sd[i] < 0) down += t->node_nreq[c];
+    }
+    for (size_t i = 0; i < kids[x].size(); ++i) {
+      const int32_t c = kids[x][i];
+      const int64_t u = up - (sd[i] > 0 ? t->node_nreq[c] : 0), dn = down - (sd[i] < 0 ? t->node_nreq[c] : 0);
+      const int sc = sd[i], ss = (u > dn) - (u < dn);
+      if (sc != 0 && ss != 0 && sc != ss && (int64_t)t->node_start[c] <= split_waste) {
+        moved[c] = 1;
+        any = true;
+      }
+    }
+  }
+  if (!any) return false;
+  std::vector<int32_t> gid(NN, 0);
+  int32_t k = 0;
+  for (int32_t x = 0; x < NN; ++x)
+    if (moved[x]) gid[x] = ++k;
+  for (int32_t r = 0; r < R; ++r) {
+    t->req_group[r] = 0;
+    for (int64_t p = t->req_path_off[r]; p < t->req_path_off[r + 1]; ++p)
+      if (gid[t->req_path_nodes[p]]) {
+        t->req_group[r] = gid[t->req_path_nodes[p]];
+        break;
+      }
+  }
+  return true;
 }
 
 // ---------------------------------------------------------------------------
@@ -992,6 +1028,7 @@ int blend_tree_get_view(const blend_tree* t, blend_tree_view* v) {
   v->req_class = t->req_class.data();
   v->req_dfs_rank = t->req_dfs_rank.data();
   v->req_global_id = t->global_id.data();
+  v->req_group = t->req_group.data();
   return BLEND_OK;
 }
 

@@ -19,7 +19,7 @@ from tests.plan_sim import simulate
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 KEYS = ["n_nodes", "node_parent", "node_start", "node_len", "node_page_off", "node_class",
         "node_key_cu", "node_key_mu", "node_first_req", "node_nreq", "page_table", "req_path_off",
-        "req_path_nodes", "req_q_off", "req_class", "req_dfs_rank", "req_global_id"]
+        "req_path_nodes", "req_q_off", "req_class", "req_dfs_rank", "req_global_id", "req_group"]
 
 
 def test_exports_every_header_symbol():
@@ -54,6 +54,34 @@ def test_descriptors_random(seed):
     t = build_tree(w, free_pages=free, **{"rows_min": 128, "min_sep_len": 128, **kw})
     _same(t.view(), v_o)
     assert t.dump() == OT.dump(v_o, w)
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_descriptors_alg2_split(seed):
+    """Alg. 2 conditional node splitting (split_waste = t): bit-exact with the oracle,
+    and the plan of the split tree still computes exact attention (CPU plan interpreter)."""
+    w = random_workload(500 + seed, hq=4, hkv=2, tok_hi=1004 if seed % 3 == 0 else 32000, max_seg=30,
+                        n_req=int(10 + seed))
+    t_w = [4, 20, 60, 10 ** 6][seed % 4]
+    v_o = OT.build(w, split_waste=t_w)
+    t = build_tree(w, split_waste=t_w)
+    _same(t.view(), v_o)
+    assert t.dump() == OT.dump(v_o, w)
+    if seed % 4 == 1:
+        out, lse, written, _ = simulate(w, t)
+        ref = A.attention_workload(w)
+        qo = np.concatenate([[0], np.cumsum(w.q_len)])
+        for r, (O, L) in ref.items():
+            assert np.max(np.abs(out[qo[r]:qo[r + 1]] - O)) < 1e-10
+
+
+def test_alg2_relocates_somewhere():
+    moved = 0
+    for seed in range(16):
+        w = random_workload(500 + seed, hq=4, hkv=2, tok_hi=1004 if seed % 3 == 0 else 32000, max_seg=30,
+                            n_req=int(10 + seed))
+        moved += int((OT.build(w, split_waste=10 ** 6)["req_group"] > 0).sum())
+    assert moved > 0
 
 
 @pytest.mark.parametrize("name", ["c1a", "c1b", "c1c", "c1d", "c2", "c3", "c5"])

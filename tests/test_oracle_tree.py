@@ -416,3 +416,58 @@ def test_root_key_adds_disjoint_subtrees_and_sharing_ratio():
     Pm, HL4 = 8_030_261_248, 4 * 4096 * 32
     s = T.sharing_ratio(w2, v2)
     assert s == pytest.approx(1 - (2 * Pm * 50 + HL4 * 4 * 2500) / (4 * (2 * Pm * 50 + HL4 * 2500)), rel=1e-12)
+
+
+# ---------------------------------------------------------------------------
+# Alg. 2 conditional node splitting (body missing -> reading #24)
+# ---------------------------------------------------------------------------
+def _fig_overview(prefix_len=50):
+    """P:349's scenario: request #2 (low density, long output) shares a prefix with the
+    compute-intensive #1 and #3; another subtree (#4, #5) sits between them in density."""
+    rng = np.random.default_rng(11)
+    pa = list(rng.integers(1000, 32000, prefix_len))
+    pb = list(rng.integers(1000, 32000, 60))
+    tail = lambda: list(rng.integers(1000, 32000, 40))    # noqa: E731
+    paths = [pa + tail(), pa + tail(), pa + tail(), pb + tail(), pb + tail()]
+    n = [len(x) for x in paths]
+    return from_paths(paths, p=n, d=[2, 16384, 2, 300, 300])
+
+
+def test_alg2_relocates_figure_outlier():
+    w = _fig_overview()
+    v0 = T.build(w)
+    assert list(v0["req_group"]) == [0] * 5
+    v = T.build(w, split_waste=50)
+    # request #2 (index 1) is relocated: before, its 16K-token output dragged its
+    # compute-intensive siblings' subtree below the other one; after, the siblings lead the
+    # DFS order and the outlier is rightmost, so densities fall left to right
+    assert list(v["req_group"]) == [0, 1, 0, 0, 0]
+    assert [int(x) for x in v0["dfs_order"]] == [3, 4, 0, 2, 1]
+    assert [int(x) for x in v["dfs_order"]] == [0, 2, 3, 4, 1]
+    from fractions import Fraction as Fr
+    tops = [i for i in range(v["n_nodes"]) if v["node_parent"][i] < 0]
+    rhos = [Fr(v["cu"][i], v["mu"][i]) for i in tops]
+    assert rhos == sorted(rhos, reverse=True) and len(tops) == 3
+    # its 50-token shared prefix is duplicated: +50 tokens of nodes, and the batch's GEMM
+    # tokens grow by exactly those 50 recomputed prompt tokens ("recomputation waste")
+    assert int(v["node_len"].sum()) - int(v0["node_len"].sum()) == 50
+    assert T.root_key(v)[0] - T.root_key(v0)[0] == 2 * int(w.model_params) * 50
+    assert T.root_key(v)[1] == T.root_key(v0)[1]
+    # every request still ends exactly once (leaf multiset unchanged)
+    assert sorted(int(x) for x in v["dfs_order"]) == list(range(5))
+
+
+def test_alg2_threshold_and_off():
+    w = _fig_overview()
+    assert list(T.build(w, split_waste=49)["req_group"]) == [0] * 5     # waste 50 > t
+    v0, v1 = T.build(w), T.build(w, split_waste=0)
+    assert T.dump(v0, w) == T.dump(v1, w)
+
+
+def test_alg2_no_outlier_when_siblings_agree():
+    # all children on the same side of rho(rt): nothing moves whatever the threshold
+    rng = np.random.default_rng(12)
+    pa = list(rng.integers(1000, 32000, 30))
+    paths = [pa + list(rng.integers(1000, 32000, 10)) for _ in range(3)] + [list(rng.integers(1000, 32000, 40))]
+    w = from_paths(paths, p=[len(x) for x in paths], d=[2, 3, 4, 20000])
+    assert list(T.build(w, split_waste=10 ** 9)["req_group"]) == [0] * 4
