@@ -534,6 +534,40 @@ def run_ours(args):
     return 0
 
 
+def run_whole(args):
+    """NEXT-2 whole-workload line (P:459 / P:480): the dual scanner's blended batches of the
+    whole C4 workload, a systematic sample of steps timed through blend_attention; the DFS
+    order under the same memory as the reference policy."""
+    import torch
+
+    import paper_2411_16102_b200 as B
+    from harness.whole import whole_run
+    from synth import workloads as W
+    if int(os.environ.get("RANK", "0")) != 0:
+        return 0
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    B.lib()
+    t = float(args.workload.split("_t")[1]) if "_t" in args.workload else 1.0
+    w = W.c4_grid(t=t, whole=True)
+    res = {}
+    for pol in (B.SCHED_DUAL, B.SCHED_DFS):
+        res["dual" if pol == B.SCHED_DUAL else "dfs"] = whole_run(
+            w, args.mem_tokens, n_sample=args.whole_samples, policy=pol, reps=3)
+    d = res["dual"]
+    line = {"metric": "whole-workload attention tokens/s (dual-scanner batches, sampled steps)",
+            "value": d["tokens_per_s"], "unit": "tokens/s", "n_gpus": 1, "higher_is_better": True,
+            "dtype": "bf16", "data": "synthetic", "scaling": "strong", "vs_baseline": None,
+            "config": {"workload": w.name, "requests": w.n_req, "mem_tokens": args.mem_tokens,
+                       "note": "one layer; KV memory M in tokens of the whole model (B200: ~1.2M for "
+                               "Llama-3.1-8B at 131072 B/token)"},
+            "dual": d, "dfs": res["dfs"],
+            "sharing_vs_optimal": {"dual": d["sharing_vs_optimal"], "dfs": res["dfs"]["sharing_vs_optimal"],
+                                   "paper": ">97% (P:480), >99% (P:383)"},
+            "speedup_vs_dfs": d["tokens_per_s"] / res["dfs"]["tokens_per_s"]}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -552,6 +586,10 @@ def main():
                     help="N > 1: N independent copies of the recipe (weak scaling) instead of one batch")
     ap.add_argument("--no-check", action="store_true",
                     help="N > 1: skip rank 0's check of the gathered result against the 1-GPU run")
+    ap.add_argument("--whole", action="store_true",
+                    help="NEXT-2: whole-workload run of the C4 recipe through the dual-scanner batch former")
+    ap.add_argument("--mem-tokens", type=int, default=1_200_000, help="--whole: KV memory M in tokens")
+    ap.add_argument("--whole-samples", type=int, default=24, help="--whole: steps timed per policy")
     ap.add_argument("--tp", action="store_true",
                     help="head-parallel replicas (NEXT-4): each rank takes Hkv/N kv heads of the whole batch")
     ap.add_argument("--tp-ranks", type=int, default=0,
@@ -562,6 +600,8 @@ def main():
         raise SystemExit("--warmup must be >= 3")
     if args.impl == "reference":
         return run_reference(args)
+    if args.whole:
+        return run_whole(args)
     return run_ours(args)
 
 

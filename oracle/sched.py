@@ -24,10 +24,15 @@ are DESIGN.md §3 #25-#31.
     admits one request regardless, so one oversized request cannot deadlock it); a side
     whose queue empties moves its cursor inward (left: L + 1, right: R - 1) and the
     partition is recomputed; a cursor that would cross the other stops.
-    On admission, the request's prompt prefix already in the runtime cache — the longest
-    common prefix with any ACTIVE request, capped at that request's materialised prompt
-    tokens (reading #28) — is counted as cached and not prefilled again (at least one
-    prompt token is always computed).
+    On admission, the request's prompt prefix shared with an ACTIVE request or with the
+    most recently completed request of either side (whose path stays cached: "only one
+    path needs to be cached for reuse") — the longest common prefix, capped at
+    that request's prompt length; active requests in admission order, then the left and
+    the right side's last completed request, the first wins ties — is reused, not
+    prefilled again (at least one prompt token is always computed): intra-batch prefix
+    sharing (P:11 "exactly-once computation of shared prefixes"; reading #28).  The request then waits (no prefill entry) until its
+    provider has materialised the reused prefix — in the same step at the earliest, the
+    provider coming first in the batch.
  5. Step batch: every active request contributes one entry (admission order): while its
     prompt is not fully materialised, a chunked-prefill step of q = min(chunk, remaining,
     left-over prefill budget) tokens (P:15 chunked prefill; the per-step budget is served
@@ -136,6 +141,8 @@ def schedule(w, view, mem_tokens: int, chunk: int = 512, step_budget: int = 8192
     order, side_of = [], [0] * R
     cached_total = 0
     steps, mleft_steps = [], []
+    dep = {}                             # request -> (provider request, prefix it needs)
+    last_done = [-1, -1]                 # the most recently completed request of each side
     while True:
         # ---- admission (step 4)
         for s in ((0,) if policy == "dfs" else (0, 1)):
@@ -161,10 +168,14 @@ def schedule(w, view, mem_tokens: int, chunk: int = 512, step_budget: int = 8192
                 if used[s] > 0 and used[s] + fp > cap:
                     break
                 q_s.pop(0)
-                cached = 0
-                for a, _, mat, _ in active:
-                    cached = max(cached, min(_lcp(view, w, r, a), mat))
+                cached, prov = 0, -1
+                for a in [e[0] for e in active] + [x for x in last_done if x >= 0]:
+                    c = min(_lcp(view, w, r, a), p[a])
+                    if c > cached:
+                        cached, prov = c, a
                 cached = min(cached, max(0, p[r] - 1))
+                if cached > 0:
+                    dep[r] = (prov, cached)
                 cached_total += cached
                 used[s] += fp
                 active.append([r, s, cached, 0])
@@ -175,9 +186,14 @@ def schedule(w, view, mem_tokens: int, chunk: int = 512, step_budget: int = 8192
         # ---- one step (step 5)
         batch = []
         budget = step_budget
+        mat_of = {e[0]: e for e in active}
         for e in active:
             r, s, mat, dec = e
             if mat < p[r]:
+                if r in dep:
+                    a, need = dep[r]
+                    if a in mat_of and mat_of[a][2] < need:
+                        continue                     # waiting for the provider's prefix
                 q = min(chunk, p[r] - mat, budget)
                 if q <= 0:
                     continue
@@ -194,6 +210,7 @@ def schedule(w, view, mem_tokens: int, chunk: int = 512, step_budget: int = 8192
             r, s, mat, dec = e
             if mat >= p[r] and dec >= d[r]:
                 used[s] -= p[r] + d[r]
+                last_done[s] = r
             else:
                 keep.append(e)
         active = keep

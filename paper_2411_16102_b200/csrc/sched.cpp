@@ -11,7 +11,7 @@
 //      by  M_L + M_R = M,  M_L rho(R_L) + M_R rho(R_R) = M rho(rt) whenever a
 //      cursor moves;
 //   3. continuous batching per side with chunked prefill and a runtime
-//      prefix cache of the active requests.
+//      prefix cache of the active requests plus each side's last completed path.
 // The readings of what §4.4 leaves open are DESIGN.md §3 #25-#31.
 #include <algorithm>
 #include <cstring>
@@ -161,6 +161,8 @@ int32_t lcp(const blend_tree* t, int32_t a, int32_t b) {
 struct Active {
   int32_t r, side;
   int64_t mat, dec;   // materialised prompt tokens, decodes done
+  int32_t prov;       // request providing the reused prompt prefix (-1: none)
+  int64_t need;       // prefix length it must have materialised first
 };
 
 int schedule_impl(const blend_tree* t, const blend_sched_args* a, blend_schedule* S) {
@@ -201,6 +203,8 @@ int schedule_impl(const blend_tree* t, const blend_sched_args* a, blend_schedule
   repartition();
   int64_t used[2] = {0, 0};
   std::vector<Active> active;
+  std::vector<int32_t> slot(R, -1);   // index of an active request in `active`, -1 otherwise
+  int32_t last_done[2] = {-1, -1};    // each side's most recently completed request
   S->side.assign(R, 0);
   const int64_t max_steps = a->max_steps > 0 ? a->max_steps : INT64_MAX;
   for (int64_t step = 0; step < max_steps; ++step) {
@@ -242,12 +246,26 @@ int schedule_impl(const blend_tree* t, const blend_sched_args* a, blend_schedule
         const int64_t fp = (int64_t)p[r] + d[r];
         if (used[s] > 0 && used[s] + fp > cap) break;
         ++*pos;
+        // prefix sharing: reuse the longest prompt prefix shared with an active request or
+        // with a side's most recently completed one (its path stays cached), capped at
+        // that request's prompt; active requests in admission order first, ties to the first
         int64_t cached = 0;
-        for (const Active& e : active) cached = std::max<int64_t>(cached, std::min<int64_t>(lcp(t, r, e.r), e.mat));
+        int32_t prov = -1;
+        auto consider = [&](int32_t a2) {
+          const int64_t c = std::min<int64_t>(lcp(t, r, a2), p[a2]);
+          if (c > cached) {
+            cached = c;
+            prov = a2;
+          }
+        };
+        for (const Active& e : active) consider(e.r);
+        for (int sd = 0; sd < 2; ++sd)
+          if (last_done[sd] >= 0) consider(last_done[sd]);
         cached = std::min<int64_t>(cached, std::max<int64_t>(0, (int64_t)p[r] - 1));
         S->cached_prompt_tokens += cached;
         used[s] += fp;
-        active.push_back({r, s, cached, 0});
+        active.push_back({r, s, cached, 0, cached > 0 ? prov : -1, cached});
+        slot[r] = (int32_t)active.size() - 1;
         S->order.push_back(r);
         S->side[r] = (uint8_t)s;
       }
@@ -257,6 +275,8 @@ int schedule_impl(const blend_tree* t, const blend_sched_args* a, blend_schedule
     int64_t budget = budget0;
     for (Active& e : active) {
       if (e.mat < p[e.r]) {
+        // wait until the provider (earlier in the batch) has materialised the reused prefix
+        if (e.prov >= 0 && slot[e.prov] >= 0 && active[slot[e.prov]].mat < e.need) continue;
         const int64_t q = std::min<int64_t>(std::min<int64_t>(chunk, p[e.r] - e.mat), budget);
         if (q <= 0) continue;
         budget -= q;
@@ -275,8 +295,14 @@ int schedule_impl(const blend_tree* t, const blend_sched_args* a, blend_schedule
     S->m_left.push_back(m_left);
     size_t k = 0;
     for (const Active& e : active) {
-      if (e.mat >= p[e.r] && e.dec >= d[e.r]) used[e.side] -= (int64_t)p[e.r] + d[e.r];
-      else active[k++] = e;
+      if (e.mat >= p[e.r] && e.dec >= d[e.r]) {
+        used[e.side] -= (int64_t)p[e.r] + d[e.r];
+        slot[e.r] = -1;
+        last_done[e.side] = e.r;
+      } else {
+        slot[e.r] = (int32_t)k;
+        active[k++] = e;
+      }
     }
     active.resize(k);
   }

@@ -179,7 +179,8 @@ def c4_counts(t: float):
     return tuple(int(x) for x in e["counts"])
 
 
-def c4_grid(seed: int = 4, t: float = 1.0, counts=None, chunk: int = 512, n_total: int = 40000) -> Workload:
+def c4_grid(seed: int = 4, t: float = 1.0, counts=None, chunk: int = 512, n_total: int = 40000,
+            whole: bool = False) -> Workload:
     """configs[3]: the paper's A.1 grid recipe with synthetic lengths —
     40,000 requests mixing BurstGPT-like (prompt LN(600, 0.7) in [16, 4096], output
     LN(256, 0.7) in [1, 4096]), OpenVid-like (caption LN(100, 0.4) in [16, 512],
@@ -191,7 +192,9 @@ def c4_grid(seed: int = 4, t: float = 1.0, counts=None, chunk: int = 512, n_tota
     Each class draws from its own random stream, so the first n requests of a class do
     not depend on the other classes' counts (the count solve is monotone).
     Snapshot: every request sits at a uniformly random step of its lifetime
-    (ceil(p_private / 512) prefill chunks, then d decodes); shared prefixes cached."""
+    (ceil(p_private / 512) prefill chunks, then d decodes); shared prefixes cached.
+    whole=True: the whole offline workload instead (NEXT-2): each path is the request's
+    full prompt (p = path length), for the dual-scanner batch former."""
     nb, nv, nm = c4_counts(t) if counts is None else counts
     rs = np.random.default_rng([seed, 0])
     sys_b, sys_v, sys_m = _toks(rs, 128), _toks(rs, 128), _toks(rs, 128)
@@ -199,6 +202,8 @@ def c4_grid(seed: int = 4, t: float = 1.0, counts=None, chunk: int = 512, n_tota
     paths, q, p, d = [], [], [], []
 
     def snapshot(rng, shared, priv_len, dd):
+        if whole:
+            return np.concatenate([shared, _toks(rng, priv_len)]), 1
         n_chunks = -(-priv_len // chunk)
         k = int(rng.integers(0, n_chunks + dd))
         if k < n_chunks:
@@ -232,10 +237,38 @@ def c4_grid(seed: int = 4, t: float = 1.0, counts=None, chunk: int = 512, n_tota
         path, qq = snapshot(rm, shared, qm, 2)
         paths.append(path); q.append(qq); p.append(len(shared) + qm); d.append(2)
     order = np.random.default_rng([seed, 9]).permutation(len(paths))   # arrival order is not tree order
-    w = _pack(f"c4_grid_t{t:.1f}_s0.5", seed, [paths[i] for i in order], np.asarray(q)[order],
+    w = _pack(f"c4_{'whole' if whole else 'grid'}_t{t:.1f}_s0.5", seed, [paths[i] for i in order], np.asarray(q)[order],
               np.asarray(p)[order], np.asarray(d)[order], dict(LLAMA8B), "bf16", 64)
     w.meta.update(counts=(nb, nv, nm), t=t)
     return w
+
+
+def generated_tokens(w: Workload, r: int, n: int) -> np.ndarray:
+    """Synthetic output tokens 0..n-1 of request r (whole-workload runs): a counter hash of
+    (seed, global request id, index), ids in [TOK_LO, TOK_HI)."""
+    from synth import values as V
+    ctr = (np.uint64(w.gid(r)) << np.uint64(24)) + np.arange(n, dtype=np.uint64)
+    z = V.mix(np.uint64(w.seed ^ 0x6A09E667F3BCC909) ^ V.mix(ctr))
+    return (TOK_LO + (z % np.uint64(TOK_HI - TOK_LO)).astype(np.int64)).astype(np.int32)
+
+
+def step_workload(w: Workload, req, n_cached, q, name: str = "step") -> Workload:
+    """The blended batch of one scheduled step: request req[i] with cached path length
+    n_cached[i] (its prompt prefix, then its generated tokens) and q[i] query tokens."""
+    paths = []
+    for r, n in zip(req, n_cached):
+        r, n = int(r), int(n)
+        pr = w.path(r)
+        paths.append(pr[:n] if n <= len(pr) else np.concatenate([pr, generated_tokens(w, r, n - len(pr))]))
+    tok_off = np.zeros(len(paths) + 1, dtype=np.int64)
+    tok_off[1:] = np.cumsum([len(x) for x in paths])
+    gid = np.asarray([w.gid(int(r)) for r in req], dtype=np.int64)
+    return Workload(name=name, seed=w.seed, num_q_heads=w.num_q_heads, num_kv_heads=w.num_kv_heads,
+                    head_dim=w.head_dim, kv_dtype=w.kv_dtype, page_size=w.page_size,
+                    model_params=w.model_params, hidden=w.hidden, layers=w.layers,
+                    tokens=np.concatenate(paths).astype(np.int32), tok_off=tok_off,
+                    q_len=np.asarray(q, dtype=np.int32), prompt_len=w.prompt_len[np.asarray(req)],
+                    out_len=w.out_len[np.asarray(req)], scale_q=w.scale_q, global_id=gid)
 
 
 def concat(workloads: List[Workload], name: str) -> Workload:

@@ -122,3 +122,22 @@ def test_dual_scanner_blends_both_sides():
     assert {r < 20 for r, _, _ in first} == {True, False}          # both sides in the first batch
     od = OS.schedule(w, v, 2000, chunk=64, step_budget=4096, policy="dfs")
     assert {r < 20 for r, _, _ in od["steps"][0]} == {True}
+
+
+def test_c4_whole_workload_sharing_and_blending():
+    """The C4 grid as a whole offline workload (40,000 requests, full prompts) on one B200's
+    KV capacity (1.2M tokens): the dual scanner keeps > 97 % of the optimal prefix sharing
+    (">99 %") and, by blending both ends of the sorted tree, needs fewer
+    steps than the DFS order for the same tokens."""
+    from synth import workloads as W
+    w = W.c4_grid(whole=True)
+    t = build_tree(w)
+    dual = t.schedule(1_200_000, policy=B.SCHED_DUAL)
+    dfs = t.schedule(1_200_000, policy=B.SCHED_DFS)
+    assert dual["cached_prompt_tokens"] >= 0.97 * dual["optimal_cached_tokens"]
+    assert dfs["cached_prompt_tokens"] >= 0.97 * dfs["optimal_cached_tokens"]
+    assert sorted(dual["order"]) == list(range(w.n_req))
+    assert dual["n_steps"] < dfs["n_steps"]
+    # both sides are in use from the first step (the memory partition of P:362-368)
+    first = dual["req"][dual["step_off"][0]:dual["step_off"][1]]
+    assert set(dual["side"][first].tolist()) == {0, 1}
