@@ -360,3 +360,40 @@ def test_degenerate_shapes(case, path, kw):
     db.run(path=path)
     torch.cuda.synchronize()
     _cmp(w, db)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_alg2_split_trees(seed):
+    """NEXT-3: trees rebuilt by Alg. 2 (relocated subtrees with duplicated prefix pages) give
+    the same attention (P:346-351 changes descriptors, not the attention definition)."""
+    w = random_workload(600 + seed, hq=8, hkv=2, d=128, kv_dtype="bf16", page_size=64, max_seg=300,
+                        n_req=24, tok_hi=1003 if seed == 0 else 32000)
+    for t_w in (64, 10 ** 6):
+        db = device_batch(w, tree_kw=dict(split_waste=t_w))
+        db.run()
+        torch.cuda.synchronize()
+        _cmp(w, db)
+
+
+def test_scheduled_steps_parity():
+    """NEXT-2: blended batches formed by the dual scanner from a small whole workload
+    (full prompts, mixed output lengths) are ordinary attention steps: sampled steps
+    (prefill chunks next to decodes, prefixes reused from other requests) match the oracle."""
+    from synth.workloads import step_workload
+    from harness.run import build_tree
+    rng = np.random.default_rng(9)
+    sysp = list(rng.integers(1000, 32000, 200))
+    paths = [sysp + list(rng.integers(1000, 32000, int(rng.integers(50, 700)))) for _ in range(40)]
+    from tests.helpers import from_paths
+    w = from_paths(paths, p=[len(x) for x in paths], d=[2] * 20 + [400] * 20, hq=32, hkv=8, dim=128,
+                   page_size=64, kv_dtype="bf16")
+    sched = build_tree(w).schedule(6000, chunk=256, step_budget=1024)
+    so = sched["step_off"]
+    S = sched["n_steps"]
+    for s in sorted({0, 1, 3, S // 3, S // 2, S - 1}):
+        a, b = int(so[s]), int(so[s + 1])
+        sw = step_workload(w, sched["req"][a:b], sched["n_cached"][a:b], sched["q"][a:b])
+        db = device_batch(sw)
+        db.run()
+        torch.cuda.synchronize()
+        _cmp(sw, db)
