@@ -21,7 +21,8 @@ from typing import List, Optional, Sequence, Tuple
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libblend.so")
+# BLEND_LIB: a diagnostics build of the same sources (compile.py with BLEND_DEFINES)
+LIB_PATH = os.environ.get("BLEND_LIB") or os.path.join(_HERE, "libblend.so")
 
 OK, EINVAL, EMALFORMED, ENOSPC, ECUDA, ENOMEM, EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
 BF16, F32 = 0, 1

@@ -13,8 +13,15 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-BUILD = os.path.join(HERE, "_build")
-LIB = os.path.join(HERE, "libblend.so")
+# BLEND_DEFINES="A=1 B=2" builds a diagnostics variant (trace stamps, knobs) into
+# _build_<tag>/ and libblend_<tag>.so (tag = BLEND_TAG, default "diag"); load it with
+# BLEND_LIB=<path>.  The default build has no extra defines.
+# BLEND_SRC_OVERRIDE="dense.cu=/path/to/other.cu" swaps one source file (A/B builds).
+DEFINES = os.environ.get("BLEND_DEFINES", "").split()
+OVERRIDE = dict(kv.split("=", 1) for kv in os.environ.get("BLEND_SRC_OVERRIDE", "").split() if "=" in kv)
+TAG = os.environ.get("BLEND_TAG", "diag") if (DEFINES or OVERRIDE) else ""
+BUILD = os.path.join(HERE, "_build" + (f"_{TAG}" if TAG else ""))
+LIB = os.path.join(HERE, f"libblend_{TAG}.so" if TAG else "libblend.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC",
@@ -33,13 +40,13 @@ def _newer(src_paths, dst):
 
 
 def _compile(src, verbose):
-    path = os.path.join(CSRC, src)
+    path = OVERRIDE.get(src, os.path.join(CSRC, src))
     obj = os.path.join(BUILD, src + ".o")
     deps = [path] + [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith((".h", ".cuh"))] \
         + [os.path.join(ROOT, "include", "blend.h")]
     if not _newer(deps, obj):
         return obj
-    cmd = [NVCC] + COMMON + ARCH + ["-Xptxas", "-v" if verbose else "-O3", "-c", path, "-o", obj]
+    cmd = [NVCC] + COMMON + [f"-D{d}" for d in DEFINES] + ARCH + ["-Xptxas", "-v" if verbose else "-O3", "-c", path, "-o", obj]
     if src.endswith(".cpp"):
         cmd = ["g++", "-std=c++17", "-O3", "-g", "-fPIC", "-Wall", "-I", os.path.join(ROOT, "include"),
                "-I", CSRC, "-c", path, "-o", obj]

@@ -1,0 +1,10 @@
+#!/bin/bash
+# round-2 pass e: dense epilogue warpgroup -- parity, C4/C5/C2 bench, per-unit trace, ncu full of C4 dense
+OUT=gpurun_out/r2e; mkdir -p $OUT
+NCU=/usr/local/cuda/bin/ncu
+python -m paper_2411_16102_b200.compile > $OUT/build.log 2>&1 || { echo build failed; tail $OUT/build.log; exit 1; }
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x 2>&1 | tail -3
+for W in c4 c5 c2; do timeout 300 python bench.py --workload $W --steps 10 --warmup 3 --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 > $OUT/bench_$W.json; python -c "
+import json,sys; d=json.loads(open('$OUT/bench_$W.json').read()); print('$W', d['ms_per_step'], d['passes_ms'], d['clocks']['sm_mhz'])"; done
+BLEND_LIB=paper_2411_16102_b200/libblend_tu.so timeout 300 python scripts/trace_dense.py c4 > $OUT/trace_units_c4.txt 2>&1; head -16 $OUT/trace_units_c4.txt
+timeout 900 $NCU --set full --clock-control none --import-source on -k regex:dense_kernel -s 3 -c 1 -o $OUT/full_c4_dense python bench.py --workload c4 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/ncu_c4_dense.log 2>&1; tail -2 $OUT/ncu_c4_dense.log; ls -la $OUT
