@@ -43,7 +43,6 @@ namespace blend {
 
 #ifndef DN_NSTAGE128
 #define DN_NSTAGE128 4     // K/V ring stages at D = 128 (64 keys each)
-#define DN_STAGED_EPI 1    // epilogue through the smem staging tile (else per-thread row stores)
 #endif
 #ifndef BLEND_TRACE_WARPS
 #define BLEND_TRACE_WARPS 0    // 1: per-warp P hand-off stamps for blocks 20..23 of the first unit
@@ -77,7 +76,7 @@ __host__ __device__ inline DenseSmem dense_layout(int D) {
   L.nstage = D == 128 ? DN_NSTAGE128 : 8;
   L.bar = L.stage0 + L.nstage * L.stage_stride;
   L.stg = L.bar + 512;                    // epilogue staging: per softmax warp 32 rows x 128 B
-  L.total = L.stg + (DN_STAGED_EPI ? 8 * 4096 : 0);
+  L.total = L.stg + 8 * 4096;
   return L;
 }
 
@@ -562,39 +561,17 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       const float inv = l > 0.f ? 1.f / l : 0.f;
       const float lse2 = l > 0.f ? m_use + log2f(l) : -INFINITY;
       // O / l leaves through a per-warp smem staging tile (XOR-swizzled 16-B units, no
-      // bank conflicts), so that every global store instruction writes whole 128-B row
-      // segments (4 rows per instruction) instead of 32 scattered 16-B pieces.
-      // Row kinds: 2 = fp32 partial row, 1 = bf16 output row (DIRECT), 0 = nothing.
-      if (!DN_STAGED_EPI) {
-        // each thread writes its own row (16-B stores)
-#pragma unroll 1
-        for (int hh = 0; hh < D / 64; ++hh) {
-          uint32_t ov2[64];
-          ptx::tmem_ld32(tmem + lane_base + col_o + hh * 64, ov2);
-          ptx::tmem_ld32(tmem + lane_base + col_o + hh * 64 + 32, ov2 + 32);
-          ptx::tmem_wait_ld();
-          if (tgt == PM_DIRECT) {
-            char* dst = reinterpret_cast<char*>(p.out) + (((int64_t)token * p.hq + head) * D + hh * 64) * 2;
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-              ptx::stg128u(dst + u * 16, make_uint4(
-                  ptx::pack_bf16(__uint_as_float(ov2[8 * u]) * inv, __uint_as_float(ov2[8 * u + 1]) * inv),
-                  ptx::pack_bf16(__uint_as_float(ov2[8 * u + 2]) * inv, __uint_as_float(ov2[8 * u + 3]) * inv),
-                  ptx::pack_bf16(__uint_as_float(ov2[8 * u + 4]) * inv, __uint_as_float(ov2[8 * u + 5]) * inv),
-                  ptx::pack_bf16(__uint_as_float(ov2[8 * u + 6]) * inv, __uint_as_float(ov2[8 * u + 7]) * inv)));
-          } else if (tgt >= 0) {
-            float* dst = p.ws_o + ((int64_t)tgt * p.hq + head) * D + hh * 64;
-#pragma unroll
-            for (int u = 0; u < 16; ++u)
-              ptx::stg128(dst + 4 * u, make_float4(__uint_as_float(ov2[4 * u]) * inv, __uint_as_float(ov2[4 * u + 1]) * inv,
-                                                   __uint_as_float(ov2[4 * u + 2]) * inv, __uint_as_float(ov2[4 * u + 3]) * inv));
-          }
-        }
-      } else {
+      // bank conflicts), so that every global store instruction writes whole row
+      // segments of 4 rows instead of 32 scattered pieces.  Row kinds: 2 = fp32 partial
+      // row, 1 = bf16 output row (DIRECT), 0 = nothing.  A warp whose rows are all bf16
+      // outputs (or nothing) stages 64 columns as bf16 per pass (one 128-B line per row:
+      // every STG.128 writes 4 whole lines); a warp with partial rows stages 32 fp32
+      // columns per pass.
+      {
         const int kind = tgt == PM_DIRECT ? 1 : (tgt >= 0 ? 2 : 0);
         char* rowp = kind == 1 ? reinterpret_cast<char*>(p.out) + ((int64_t)token * p.hq + head) * D * 2
                    : kind == 2 ? reinterpret_cast<char*>(p.ws_o + ((int64_t)tgt * p.hq + head) * D) : nullptr;
-        const uint32_t stg = ptx::smem_u32(smem + L.stg + (DN_STAGED_EPI ? (warp - 4) * 4096 : 0));
+        const uint32_t stg = ptx::smem_u32(smem + L.stg + (warp - 4) * 4096);
         const int k8 = lane & 7;
         char* rp[8];
         int rk[8];
@@ -604,9 +581,9 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
           rp[s_] = reinterpret_cast<char*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(rowp), rr));
           rk[s_] = __shfl_sync(0xffffffffu, kind, rr);
         }
-        // TMEM column loads two chunks at a time (one wait per 64 columns; 128 columns
-        // at once would exceed the 168-register compile-time budget), then chunk by chunk
-        // through the staging tile
+        const bool all_bf16 = __all_sync(0xffffffffu, kind != 2);
+        // TMEM column loads two chunks at a time (one wait per 64 columns), then through
+        // the staging tile
 #pragma unroll 1
         for (int hh = 0; hh < D / 64; ++hh) {
          uint32_t ov2[64];
@@ -614,6 +591,26 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
          ptx::tmem_ld32(tmem + lane_base + col_o + hh * 64 + 32, ov2 + 32);
          ptx::tmem_wait_ld();
          if (hh == 0 && threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 62);
+         if (all_bf16) {
+#pragma unroll
+          for (int u8 = 0; u8 < 8; ++u8) {
+            const uint32_t* o8 = ov2 + 8 * u8;
+            ptx::sts128u(stg + ptx::sw128(lane, u8),
+                         ptx::pack_bf16(__uint_as_float(o8[0]) * inv, __uint_as_float(o8[1]) * inv),
+                         ptx::pack_bf16(__uint_as_float(o8[2]) * inv, __uint_as_float(o8[3]) * inv),
+                         ptx::pack_bf16(__uint_as_float(o8[4]) * inv, __uint_as_float(o8[5]) * inv),
+                         ptx::pack_bf16(__uint_as_float(o8[6]) * inv, __uint_as_float(o8[7]) * inv));
+          }
+          __syncwarp();
+          uint4 v[8];   // all eight row segments in flight before the first store
+#pragma unroll
+          for (int s_ = 0; s_ < 8; ++s_) v[s_] = ptx::lds128u(stg + ptx::sw128(s_ * 4 + (lane >> 3), k8));
+#pragma unroll
+          for (int s_ = 0; s_ < 8; ++s_)
+            if (rk[s_] == 1) ptx::stg128u(rp[s_] + hh * 128 + k8 * 16, v[s_]);
+          __syncwarp();   // the staging tile is rewritten by the next chunk
+          continue;
+         }
 #pragma unroll
          for (int cc = 0; cc < 2; ++cc) {
           const int c = 2 * hh + cc;
