@@ -48,7 +48,7 @@ namespace blend {
 #define BLEND_TRACE_WARPS 0    // 1: per-warp P hand-off stamps for blocks 20..23 of the first unit
 #endif
 #ifndef BLEND_TRACE_UNITS
-#define BLEND_TRACE_UNITS 0    // 1: per-unit stamps (first 10 units of each CTA: start, first S, last P, epilogue end) and clock64 sums over all units
+#define BLEND_TRACE_UNITS 0    // 1: per-unit stamps (first 10 units of each CTA): start, first S, last P, epilogue end
 #endif
 #ifndef BLEND_TRACE_BLOCKS
 #define BLEND_TRACE_BLOCKS 0   // 1: per-block S / P stamps in the diagnostics trace (costs issue slots)
@@ -104,9 +104,10 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar);
   uint64_t* kv_full = bars;            // [NS <= 8]
   uint64_t* kv_empty = bars + 8;       // [NS]
-  uint64_t* s_full = bars + 16;        // [tile][buffer]
-  uint64_t* p_full = bars + 20;        // [tile][buffer]
-  uint64_t* o_done = bars + 24;        // [tile][buffer]: PV of a block that used this S buffer
+  uint64_t* s_full = bars + 16;        // [tile]: QK_t(j) done
+  uint64_t* s_free = bars + 18;        // [tile]: S_t(j) read into registers (4 softmax warps)
+  uint64_t* p_full = bars + 20;        // [tile]: P_t(j) in TMEM (4 softmax warps)
+  uint64_t* o_done = bars + 22;        // [tile]: PV_t(j) done (P_t free, O_t up to date)
   uint64_t* q_full = bars + 28;
   uint64_t* q_empty = bars + 29;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 30);
@@ -128,8 +129,9 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       ptx::mbar_init(&kv_full[s], 1);
       ptx::mbar_init(&kv_empty[s], 1);
     }
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&s_full[i], 1);
+      ptx::mbar_init(&s_free[i], 4);
       ptx::mbar_init(&p_full[i], 4);
       ptx::mbar_init(&o_done[i], 1);
     }
@@ -143,8 +145,9 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) trace_stamp(p, 1);
-  // TMEM columns: S[tile][buffer] 64 fp32 columns each at tile*128 + buffer*64 (P, bf16
-  // pairs, aliases the first 32 columns of its S buffer); O[tile] at 256 + tile*D.
+  // TMEM columns: S[tile] 64 fp32 columns at tile*64; P[tile] 32 columns (bf16 pairs) at
+  // 128 + tile*32; O[tile] at 256 + tile*D.  S and P are separate, so QK_t(j+1) may be
+  // issued as soon as the softmax has read S_t(j) into registers, before P_t(j) exists.
   // register budget: warpgroup 0 (producer, MMA, allocator, Q loader) needs few; the
   // softmax warpgroups get the rest of the CTA's launch allocation (168 x 384 = 64512 =
   // 56*128 + 224*256; setmaxnreg only redistributes the CTA's own registers).
@@ -278,9 +281,11 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (whole warp; one elected lane issues) =====================
-    // Per unit: QK(0), QK(1) for every tile, then for j = 0..nb-1 and each tile:
-    //   wait P_t(j) -> PV_t(j) (P from TMEM) -> commit o_done -> QK_t(j+2) into the S
-    //   buffer PV_t(j) just consumed (MMAs execute in issue order) -> commit s_full.
+    // Per unit, tile t:  QK_t(0);  then for j = 0..nb-1:  [j+1 < nb: wait until the
+    // softmax has read S_t(j) (s_free) -> QK_t(j+1) -> commit s_full]  for both tiles,
+    // then  wait P_t(j) -> PV_t(j) (P from TMEM, V MN-major) -> commit o_done  for both
+    // tiles, then release the K/V stage.  Every QK into S_t but a tile's first waits for
+    // the previous S_t to be read, so the next unit's QK(0) needs only its Q.
     // The warp runs all lanes so descriptors stay warp-uniform; descriptors are built
     // once per stage and advanced by adding (byte offset >> 4) to the start-address field.
     {
@@ -298,51 +303,54 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       const uint32_t stage_lo = L.stage_stride >> 4;
       const uint32_t leader = ptx::elect_one();
       uint32_t kit = 0, gu = 0;
-      uint32_t pbits = 0;               // parity of the next p_full[tile][buffer] completion (bit pi)
+      uint32_t nqk[2] = {0, 0};         // QKs issued per tile (s_free parities)
+      uint32_t npv[2] = {0, 0};         // P hand-offs consumed per tile (p_full parities)
       for (int uk = 0, ui = snake_unit(0); ui < p.n_units; ui = snake_unit(++uk)) {
         const Unit u = p.units[ui];
         const int nb = (u.entry_end - u.entry_begin + EPB - 1) / EPB;
         const int ntile = u.n_rows > 128 ? 2 : 1;
+        auto issue_qk = [&](int t, int j) {
+          if (nqk[t] > 0) {                     // S_t(previous) read by the softmax
+            ptx::mbar_wait(&s_free[t], (nqk[t] - 1) & 1);
+            ptx::tc_fence_after();
+          }
+          ++nqk[t];
+          const uint32_t qlo = t ? q_lo1 : q_lo0;
+          const uint32_t klo = k_lo0 + ((kit + j) % NS) * stage_lo;
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk)
+            ptx::umma_ss_lohi(leader, tmem + t * DN_KB, qlo + (((kk / 4) * DN_QCHUNK + (kk % 4) * 32) >> 4), q_hi,
+                              klo + (((kk / 4) * DN_KCHUNK + (kk % 4) * 32) >> 4), k_hi, IDESC_QK, kk > 0);
+          ptx::umma_commit_if(leader, &s_full[t]);
+        };
         auto wait_kv = [&](int j) {
           ptx::mbar_wait(&kv_full[(kit + j) % NS], ((kit + j) / NS) & 1);
           ptx::tc_fence_after();
         };
-        auto issue_qk = [&](int t, int j) {
-          const uint32_t qlo = t ? q_lo1 : q_lo0;
-          const uint32_t klo = k_lo0 + ((kit + j) % NS) * stage_lo;
-          const uint32_t dcol = tmem + t * 128 + (j & 1) * DN_KB;
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk)
-            ptx::umma_ss_lohi(leader, dcol, qlo + (((kk / 4) * DN_QCHUNK + (kk % 4) * 32) >> 4), q_hi,
-                              klo + (((kk / 4) * DN_KCHUNK + (kk % 4) * 32) >> 4), k_hi, IDESC_QK, kk > 0);
-          ptx::umma_commit_if(leader, &s_full[t * 2 + (j & 1)]);
-        };
         ptx::mbar_wait(q_full, gu & 1);
         ptx::tc_fence_after();
         if (gu == 0 && lane == 0) trace_stamp(p, 2);
-        for (int j = 0; j < 2 && j < nb; ++j) {
-          wait_kv(j);
-          for (int t = 0; t < ntile; ++t) issue_qk(t, j);
-        }
-        if (nb <= 2) ptx::umma_commit_if(leader, q_empty);   // every QK of the unit issued: Q may be reloaded
+        wait_kv(0);
+        for (int t = 0; t < ntile; ++t) issue_qk(t, 0);
+        if (nb == 1) ptx::umma_commit_if(leader, q_empty);   // every QK of the unit issued: Q may be reloaded
         for (int j = 0; j < nb; ++j) {
+          if (j + 1 < nb) {
+            wait_kv(j + 1);
+            for (int t = 0; t < ntile; ++t) issue_qk(t, j + 1);
+            if (j + 2 == nb) ptx::umma_commit_if(leader, q_empty);   // QK(nb-1) of every tile issued
+          }
           const uint32_t vlo = v_lo0 + ((kit + j) % NS) * stage_lo;
-          if (j + 2 < nb) wait_kv(j + 2);
           for (int t = 0; t < ntile; ++t) {
-            const int pi = t * 2 + (j & 1);
-            ptx::mbar_wait(&p_full[pi], (pbits >> pi) & 1);
-            pbits ^= 1u << pi;
+            ptx::mbar_wait(&p_full[t], npv[t] & 1);
+            ++npv[t];
             ptx::tc_fence_after();
-            const uint32_t acol = tmem + t * 128 + (j & 1) * DN_KB;
 #pragma unroll
             for (int kk = 0; kk < DN_KB / 16; ++kk)
-              ptx::umma_ts_lohi(leader, tmem + 256 + t * D, acol + kk * 8, vlo + ((kk * 16 * 128) >> 4), v_hi,
-                                IDESC_PV, (j > 0 || kk > 0) ? 1u : 0u);
-            ptx::umma_commit_if(leader, &o_done[pi]);
-            if (j + 2 < nb) issue_qk(t, j + 2);
+              ptx::umma_ts_lohi(leader, tmem + 256 + t * D, tmem + 128 + t * 32 + kk * 8, vlo + ((kk * 16 * 128) >> 4),
+                                v_hi, IDESC_PV, (j > 0 || kk > 0) ? 1u : 0u);
+            ptx::umma_commit_if(leader, &o_done[t]);
           }
-          if (j + 3 == nb) ptx::umma_commit_if(leader, q_empty);   // QK(nb-1) of every tile issued
-          ptx::umma_commit_if(leader, &kv_empty[(kit + j) % NS]);
+          ptx::umma_commit_if(leader, &kv_empty[(kit + j) % NS]);   // QK(j) and PV(j) of every tile issued
         }
         kit += nb;
         ++gu;
@@ -360,8 +368,9 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
 #if BLEND_TRACE_UNITS
     long long cu_acc[6] = {0, 0, 0, 0, 0, 0};         // clock64 sums: start->S0, S0->last P, epilogue, gap; blocks; units
     long long cu_prev_end = 0;
+    long long ph_acc[6] = {0, 0, 0, 0, 0, 0};         // per block: s_full wait, S ld, exps, PV wait, P st + arrive; blocks
 #endif
-    uint32_t scnt0 = 0, scnt1 = 0;                    // s_full completions consumed per S buffer (registers)
+    uint32_t scnt = 0, ocnt = 0;                      // s_full / o_done completions consumed (this tile)
     int2 enext[EPB];                                  // {pos0, count} of the next block's entries
     auto load_meta = [&](const Unit& un, int j) {
 #pragma unroll
@@ -402,10 +411,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       const bool warp_pad = __all_sync(0xffffffffu, !row_ok);
       load_meta(u, 0);
       for (int j = 0; j < nb; ++j, ++sb) {
-        const int buf = j & 1;
-        const uint32_t col_s = t * 128 + buf * DN_KB;
-        // key positions of this block from the stage metadata the producer wrote (the
-        // stage cannot be refilled before this block's P is consumed)
+        const uint32_t col_s = t * DN_KB, col_p = 128 + t * 32;
         // this block's {pos0, count} were loaded one block ahead (latency off the critical path)
         int2 ecur[EPB];
 #pragma unroll
@@ -421,8 +427,14 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
           vis[i] = v;
           full_vis = full_vis && (v == BOX);
         }
-        ptx::mbar_wait(&s_full[t * 2 + buf], (buf ? scnt1++ : scnt0++) & 1);   // per-buffer completion count
+#if BLEND_TRACE_UNITS
+        const long long ph0 = clock64();
+#endif
+        ptx::mbar_wait(&s_full[t], scnt++ & 1);
         ptx::tc_fence_after();
+#if BLEND_TRACE_UNITS
+        const long long ph1 = clock64();
+#endif
 #if BLEND_TRACE_UNITS
         if (threadIdx.x == 128 && uk < 10 && j == 0) trace_stamp(p, 21 + 4 * uk);
         if (j == 0) cu_s0 = clock64();
@@ -453,22 +465,42 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
 #if BLEND_TRACE_BLOCKS
         if (threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 8 + 2 * j);
 #endif
+        // A warp whose rows are all padding keeps the barrier protocol only (its P rows
+        // feed its own never-stored O rows).
+        float sv[DN_KB];
+        if (!warp_pad) {
+          ptx::tmem_ld32(tmem + lane_base + col_s, reinterpret_cast<uint32_t*>(sv));
+          ptx::tmem_ld32(tmem + lane_base + col_s + 32, reinterpret_cast<uint32_t*>(sv + 32));
+          ptx::tmem_wait_ld();
+        }
+#if BLEND_TRACE_UNITS
+        const long long ph2 = clock64();
+#endif
+        // S_t(j) is in registers: QK_t(j+1) may overwrite it
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&s_free[t]);
+        // P_t(j-1) consumed and O_t up to date: PV_t(j-1) done (needed before P_t(j) is
+        // written and before a rescale of O_t)
+        auto wait_pv = [&]() {
+          if (j > 0) {
+            ptx::mbar_wait(&o_done[t], ocnt++ & 1);
+            ptx::tc_fence_after();
+          }
+        };
         if (warp_pad) {
+          wait_pv();
           __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&p_full[t * 2 + buf]);
+          if (lane == 0) ptx::mbar_arrive(&p_full[t]);
           continue;
         }
-        float sv[DN_KB];
-        ptx::tmem_ld32(tmem + lane_base + col_s, reinterpret_cast<uint32_t*>(sv));
-        ptx::tmem_ld32(tmem + lane_base + col_s + 32, reinterpret_cast<uint32_t*>(sv + 32));
-        ptx::tmem_wait_ld();
         if (!full_vis) {
 #pragma unroll
           for (int k = 0; k < DN_KB; ++k) sv[k] = (k % BOX) < vis[k / BOX] ? sv[k] : -INFINITY;
         }
         // P = exp2(s*scale - m) on packed fp32 pairs (FFMA2/FADD2): 3 of every 4 pairs on the
-        // MUFU pipe, 1 of 4 as a polynomial on the FMA pipe; bf16 pairs -> the first 32 TMEM
-        // columns of this S buffer.
+        // MUFU pipe, 1 of 4 as a polynomial on the FMA pipe; bf16 pairs -> P_t (32 TMEM
+        // columns).
         uint32_t pk[DN_KB / 2];
         float lsum = 0.f;
         auto exps = [&](float m_use) {
@@ -505,6 +537,13 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
           exps(m_ref == -INFINITY ? 0.f : m_ref);   // -inf: a padding row (all scores masked)
           slow = __any_sync(0xffffffffu, !(lsum <= 256.f));
         }
+#if BLEND_TRACE_UNITS
+        const long long ph3 = clock64();
+#endif
+        wait_pv();
+#if BLEND_TRACE_UNITS
+        const long long ph4 = clock64();
+#endif
         if (p.stats != nullptr && lane == 0) {   // diagnostics: blocks per softmax path
           stat_add(p, STAT_DENSE_BLOCKS, 1);
           if (slow) stat_add(p, STAT_DENSE_SLOW, 1);
@@ -522,12 +561,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         const bool need = mx2 > m_ref + DN_RESCALE_T;
         if (j > 0 && __any_sync(0xffffffffu, need)) {
           if (lane == 0) stat_add(p, STAT_DENSE_RESCALE, 1);
-          // O holds PV up to block j-1: wait for it.  Parity is unambiguous because the
-          // previous completion on this barrier (PV(j-3)) is certified by s_full(j-1) and
-          // PV(j+1) cannot be issued before this block's P.
-          const int pb_ = (j - 1) & 1;
-          ptx::mbar_wait(&o_done[t * 2 + pb_], ((pb_ ? scnt1 : scnt0) - 1) & 1);
-          ptx::tc_fence_after();
+          // O holds PV up to block j-1 (wait_pv above)
           const float alpha = need ? ptx::ex2(m_ref - mx2) : 1.f;
 #pragma unroll 1
           for (int c = 0; c < D / 32; ++c) {
@@ -546,12 +580,23 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
           exps(m_ref == -INFINITY ? 0.f : m_ref);
         }
 #pragma unroll
-        for (int c = 0; c < DN_KB / 32; ++c) ptx::tmem_st16(tmem + lane_base + col_s + c * 16, pk + 16 * c);
+        for (int c = 0; c < DN_KB / 32; ++c) ptx::tmem_st16(tmem + lane_base + col_p + c * 16, pk + 16 * c);
         l += lsum;
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&p_full[t * 2 + buf]);
+        if (lane == 0) ptx::mbar_arrive(&p_full[t]);
+#if BLEND_TRACE_UNITS
+        if (!slow) {
+          const long long ph5 = clock64();
+          ph_acc[0] += ph1 - ph0;
+          ph_acc[1] += ph2 - ph1;
+          ph_acc[2] += ph3 - ph2;
+          ph_acc[3] += ph4 - ph3;
+          ph_acc[4] += ph5 - ph4;
+          ph_acc[5] += 1;
+        }
+#endif
 #if BLEND_TRACE_WARPS
         if (lane == 0 && ui == (int)blockIdx.x && j >= 20 && j < 24) trace_stamp(p, 24 + (j - 20) * 8 + (warp - 4));
 #endif
@@ -570,10 +615,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
 #endif
       // ---- epilogue: PV of the unit's last block done (MMAs complete in issue order, so
       // this also certifies every earlier PV of the unit)
-      {
-        const int lb = (nb - 1) & 1;
-        ptx::mbar_wait(&o_done[t * 2 + lb], ((lb ? scnt1 : scnt0) - 1) & 1);
-      }
+      ptx::mbar_wait(&o_done[t], ocnt++ & 1);
       ptx::tc_fence_after();
       if (threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 60);
       const float m_use = m_ref == -INFINITY ? 0.f : m_ref;
@@ -668,7 +710,10 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
     }
 #if BLEND_TRACE_UNITS
     if (threadIdx.x == 128 && p.trace != nullptr)
-      for (int i = 0; i < 6; ++i) p.trace[(size_t)blockIdx.x * 64 + 40 + i] = (unsigned long long)cu_acc[i];
+      for (int i = 0; i < 6; ++i) {
+        p.trace[(size_t)blockIdx.x * 64 + 40 + i] = (unsigned long long)cu_acc[i];
+        p.trace[(size_t)blockIdx.x * 64 + 50 + i] = (unsigned long long)ph_acc[i];
+      }
 #endif
   }
   __syncwarp();       // lane 0 of the producer / MMA warps rejoins its warp before the CTA barrier
