@@ -40,6 +40,20 @@
 #include "ptx.cuh"
 
 namespace blend {
+namespace ptx {
+// non-blocking probe of a phase (mbarrier.test_wait never suspends the thread)
+__device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+}  // namespace ptx
 
 #ifndef DN_NSTAGE128
 #define DN_NSTAGE128 4     // K/V ring stages at D = 128 (64 keys each)
