@@ -43,22 +43,6 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 }
 // Wait for the phase with the given parity.  Watchdog: a wait that exceeds 10 s is a
 // protocol bug (a hang) — trap so the launch fails with an error instead of hanging.
-// named barrier over `count` threads (a multiple of 32), with an OR reduction of `pred`
-__device__ __forceinline__ bool bar_red_or(uint32_t id, uint32_t count, bool pred) {
-  uint32_t r;
-  asm volatile(
-      "{\n\t.reg .pred p, q;\n\t"
-      "setp.ne.u32 p, %1, 0;\n\t"
-      "bar.red.or.pred q, %2, %3, p;\n\t"
-      "selp.u32 %0, 1, 0, q;\n\t}"
-      : "=r"(r)
-      : "r"((uint32_t)pred), "r"(id), "r"(count)
-      : "memory");
-  return r != 0;
-}
-__device__ __forceinline__ void bar_sync(uint32_t id, uint32_t count) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
   const uint64_t t0 = globaltimer_ns();

@@ -40,6 +40,24 @@
 #include "ptx.cuh"
 
 namespace blend {
+namespace ptx {
+// named barrier over `count` threads (a multiple of 32), with an OR reduction of `pred`
+__device__ __forceinline__ bool bar_red_or(uint32_t id, uint32_t count, bool pred) {
+  uint32_t r;
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.u32 p, %1, 0;\n\t"
+      "bar.red.or.pred q, %2, %3, p;\n\t"
+      "selp.u32 %0, 1, 0, q;\n\t}"
+      : "=r"(r)
+      : "r"((uint32_t)pred), "r"(id), "r"(count)
+      : "memory");
+  return r != 0;
+}
+__device__ __forceinline__ void bar_sync(uint32_t id, uint32_t count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+}  // namespace ptx
 
 #ifndef DN_NSTAGE128
 #define DN_NSTAGE128 4     // K/V ring stages at D = 128 (64 keys each)
@@ -54,7 +72,8 @@ namespace blend {
 #define BLEND_TRACE_BLOCKS 0   // 1: per-block S / P stamps in the diagnostics trace (costs issue slots)
 #endif
 
-constexpr int DN_THREADS = 384;
+constexpr int DN_THREADS = 640;         // 4 control warps + 16 softmax warps (2 tiles x 2 column halves x 4 lane quarters)
+constexpr int DN_REG_CTL = 48, DN_REG_SOFTMAX = 104;   // setmaxnreg: 48*128 + 104*512 <= 96*640
 constexpr int DN_KB = 64;                // keys per block (UMMA N of QK^T, K of PV)
 constexpr int DN_QCHUNK = 128 * 128;     // Q: 128 rows x 128 B (one 64-column chunk)
 constexpr int DN_KCHUNK = DN_KB * 128;   // K/V: 64 rows x 128 B
@@ -75,8 +94,8 @@ __host__ __device__ inline DenseSmem dense_layout(int D) {
   L.stage_stride = 2 * CH * DN_KCHUNK;   // K chunks then V chunks
   L.nstage = D == 128 ? DN_NSTAGE128 : 8;
   L.bar = L.stage0 + L.nstage * L.stage_stride;
-  L.stg = L.bar + 512;                    // epilogue staging: per softmax warp 32 rows x 128 B
-  L.total = L.stg + 8 * 4096;
+  L.stg = L.bar + 1024;                   // epilogue staging: per softmax warp 32 rows x 64 B
+  L.total = L.stg + 16 * 2048;
   return L;
 }
 
@@ -111,6 +130,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
   uint64_t* q_empty = bars + 29;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 30);
 
+
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) trace_stamp(p, 0);
   if (p.sched != nullptr && blockIdx.x == 0) {
@@ -130,7 +150,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
     }
     for (int i = 0; i < 4; ++i) {
       ptx::mbar_init(&s_full[i], 1);
-      ptx::mbar_init(&p_full[i], 4);
+      ptx::mbar_init(&p_full[i], 8);
       ptx::mbar_init(&o_done[i], 1);
     }
     ptx::mbar_init(q_full, 1);
@@ -149,7 +169,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
   // softmax warpgroups get the rest of the CTA's launch allocation (168 x 384 = 64512 =
   // 56*128 + 224*256; setmaxnreg only redistributes the CTA's own registers).
   if (warp < 4) {
-  ptx::setmaxnreg_dec<56>();
+  ptx::setmaxnreg_dec<DN_REG_CTL>();
   if (warp == 0) {
     // ===================== TMA producer: 64-key K/V blocks into the stage ring =====================
     // The entries of the next block (and the next unit's header) are loaded one step
@@ -255,7 +275,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         }
       }
 #pragma unroll 1
-      for (int k = 0; k < 8; ++k) {   // (the loader warp runs under setmaxnreg 56)
+      for (int k = 0; k < 8; ++k) {   // (the loader warp runs under a small setmaxnreg budget)
         const int row = lane + 32 * k;
         if (row >= nrows) break;
         uint8_t* qs = smem + ((row >> 7) ? L.q1 : L.q0);
@@ -334,10 +354,12 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
             pbits ^= 1u << pi;
             ptx::tc_fence_after();
             const uint32_t acol = tmem + t * 128 + (j & 1) * DN_KB;
+            // P: keys 0..31 (left column half) at S columns 0..15, keys 32..63 (right
+            // half) at 32..47 — each half overwrites only S columns it has read itself
 #pragma unroll
             for (int kk = 0; kk < DN_KB / 16; ++kk)
-              ptx::umma_ts_lohi(leader, tmem + 256 + t * D, acol + kk * 8, vlo + ((kk * 16 * 128) >> 4), v_hi,
-                                IDESC_PV, (j > 0 || kk > 0) ? 1u : 0u);
+              ptx::umma_ts_lohi(leader, tmem + 256 + t * D, acol + (kk >> 1) * 32 + (kk & 1) * 8,
+                                vlo + ((kk * 16 * 128) >> 4), v_hi, IDESC_PV, (j > 0 || kk > 0) ? 1u : 0u);
             ptx::umma_commit_if(leader, &o_done[pi]);
             if (j + 2 < nb) issue_qk(t, j + 2);
           }
@@ -350,17 +372,27 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
     }
   }
   } else {
-    ptx::setmaxnreg_inc<224>();
-    // ===================== softmax / epilogue (tile t) =====================
-    const int t = (warp - 4) >> 2;                    // 0 = tile A, 1 = tile B
-    const int r = threadIdx.x - 128 - 128 * t;        // row within the tile = TMEM lane
-    const uint32_t lane_base = (uint32_t)(((warp - 4) & 3) * 32) << 16;
-    const uint32_t col_o = 256 + t * D;
+    ptx::setmaxnreg_inc<DN_REG_SOFTMAX>();
+    // ===================== softmax / epilogue: tile t, column half h, lane quarter q =====================
+    // Each row (TMEM lane) of a tile is served by two warps: the left one takes keys 0..31
+    // of every 64-key block, the right one keys 32..63.  They share the running reference
+    // m_ref (identical by construction: the fast/slow decision is a 64-thread barrier
+    // reduction, and in the slow path the half maxima are exchanged through smem), keep
+    // separate row sums (added at the epilogue) and each rescales / stores its own half of
+    // O.  Splitting the columns lets one warp's TMEM and barrier latencies overlap the
+    // other's exponentials.
+    const int sw = warp - 4;                            // 0..15
+    const int t = sw >> 3;                              // 0 = tile A, 1 = tile B
+    const int h = (sw >> 2) & 1;                        // column half
+    const int q = sw & 3;                               // lane quarter (= warp % 4)
+    const int r = q * 32 + lane;                        // row within the tile = TMEM lane
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    constexpr int DH = D / 2;                           // O columns of this half
+    const uint32_t col_o = 256 + t * D + h * DH;
+    const uint32_t pair_bar = 1 + t * 4 + q;            // named barrier of the warp pair (64 threads)
+    uint8_t* my_x = smem + L.stg + sw * 2048;           // this warp's staging / exchange area
+    const uint8_t* pa_x = smem + L.stg + (sw ^ 4) * 2048;   // the partner warp's
     uint32_t sb = 0;                                  // blocks of this tile processed so far
-#if BLEND_TRACE_UNITS
-    long long cu_acc[6] = {0, 0, 0, 0, 0, 0};         // clock64 sums: start->S0, S0->last P, epilogue, gap; blocks; units
-    long long cu_prev_end = 0;
-#endif
     uint32_t scnt0 = 0, scnt1 = 0;                    // s_full completions consumed per S buffer (registers)
     int2 enext[EPB];                                  // {pos0, count} of the next block's entries
     auto load_meta = [&](const Unit& un, int j) {
@@ -379,10 +411,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       if (t == 1 && u.n_rows <= 128) continue;       // tile B idle for this unit
       const int row = 128 * t + r;                    // row within the unit
 #if BLEND_TRACE_UNITS
-      if (threadIdx.x == 128 && uk < 10) trace_stamp(p, 20 + 4 * uk);
-      const long long cu0 = clock64();
-      if (cu_prev_end != 0) cu_acc[3] += cu0 - cu_prev_end;
-      long long cu_s0 = cu0;
+      if (sw == 0 && lane == 0 && uk < 10) trace_stamp(p, 20 + 4 * uk);
 #endif
       int32_t pos = INT32_MIN, token = 0, head = 0, tgt = PM_SKIP;
       if (row < u.n_rows) {
@@ -397,41 +426,45 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       float m_ref = -INFINITY, l = 0.f;
       const bool row_ok = row < u.n_rows;
       // a warp whose 32 rows are all padding (tile B of a 129..223-row unit) skips the
-      // softmax: its P rows only feed its own (never stored) O rows, so they may hold
-      // anything; it keeps the barrier protocol
+      // softmax (both warps of its pair do: same rows); its P rows only feed its own
+      // (never stored) O rows, so they may hold anything; it keeps the barrier protocol
       const bool warp_pad = __all_sync(0xffffffffu, !row_ok);
       load_meta(u, 0);
       for (int j = 0; j < nb; ++j, ++sb) {
         const int buf = j & 1;
         const uint32_t col_s = t * 128 + buf * DN_KB;
-        // key positions of this block from the stage metadata the producer wrote (the
-        // stage cannot be refilled before this block's P is consumed)
         // this block's {pos0, count} were loaded one block ahead (latency off the critical path)
         int2 ecur[EPB];
 #pragma unroll
         for (int i = 0; i < EPB; ++i) ecur[i] = enext[i];
         if (j + 1 < nb) load_meta(u, j + 1);
-        int vis[EPB];
+        // visible keys of this half's 32: key 32h + k lies in entry (32h + k) / BOX
+        constexpr int EH = (32 + BOX - 1) / BOX;          // entries touched by one half
+        int vis[EH];
         bool full_vis = true;
 #pragma unroll
-        for (int i = 0; i < EPB; ++i) {
-          const int2 en = ecur[i];                               // {pos0, count}
-          const int a = pos < en.x ? 0 : pos - en.x + 1;          // pos = INT32_MIN for padding rows
-          const int v = a > en.y ? en.y : a;
-          vis[i] = v;
-          full_vis = full_vis && (v == BOX);
+        for (int e = 0; e < EH; ++e) {
+          const int i = (32 * h) / BOX + e;               // entry index within the block
+          const int2 en = ecur[i < EPB ? i : EPB - 1];   // {pos0, count}
+          const int a = pos < en.x ? 0 : pos - en.x + 1;  // pos = INT32_MIN for padding rows
+          const int v = a > en.y ? en.y : a;              // visible rows of the entry
+          const int off = BOX >= 64 ? 32 * h : 0;         // rows of the entry before this half
+          int vh = v - off;
+          vh = vh < 0 ? 0 : (vh > (BOX >= 64 ? 32 : BOX) ? (BOX >= 64 ? 32 : BOX) : vh);
+          vis[e] = vh;
+          full_vis = full_vis && (vh == (BOX >= 64 ? 32 : BOX));
         }
         ptx::mbar_wait(&s_full[t * 2 + buf], (buf ? scnt1++ : scnt0++) & 1);   // per-buffer completion count
         ptx::tc_fence_after();
 #if BLEND_TRACE_UNITS
-        if (threadIdx.x == 128 && uk < 10 && j == 0) trace_stamp(p, 21 + 4 * uk);
-        if (j == 0) cu_s0 = clock64();
+        if (sw == 0 && lane == 0 && uk < 10 && j == 0) trace_stamp(p, 21 + 4 * uk);
 #endif
         // Entries with count < BOX (a node's last page, padding entries): their V rows past
         // the count may hold anything, NaN included, and the PV MMA would multiply them by
-        // P = 0 -> tile A's warpgroup zeroes them before its P hand-off (the PV MMAs of both
-        // tiles are issued after it).  K rows past the count only reach masked scores.
-        if (t == 0) {
+        // P = 0 -> tile A's left-half warps zero them before their P hand-off (the PV MMAs
+        // of both tiles are issued after all 8 hand-offs).  K rows past the count only
+        // reach masked scores.
+        if (t == 0 && h == 0) {
           bool part = false;
 #pragma unroll
           for (int i = 0; i < EPB; ++i) part = part || ecur[i].y < BOX;
@@ -441,8 +474,8 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
             for (int i = 0; i < EPB; ++i) {
               const int nz = BOX - ecur[i].y;
               for (int x = r; x < nz * CH * 8; x += 128) {
-                const int row = ecur[i].y + x / (CH * 8), c = (x / 8) % CH, k16 = x % 8;
-                *reinterpret_cast<uint4*>(vst + c * DN_KCHUNK + (i * BOX + row) * 128 + k16 * 16) =
+                const int rw = ecur[i].y + x / (CH * 8), c = (x / 8) % CH, k16 = x % 8;
+                *reinterpret_cast<uint4*>(vst + c * DN_KCHUNK + (i * BOX + rw) * 128 + k16 * 16) =
                     make_uint4(0, 0, 0, 0);
               }
             }
@@ -450,35 +483,34 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
             if (r == 0) stat_add(p, STAT_TAIL_ZEROED, 1);
           }
         }
-#if BLEND_TRACE_BLOCKS
-        if (threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 8 + 2 * j);
-#endif
         if (warp_pad) {
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&p_full[t * 2 + buf]);
           continue;
         }
-        float sv[DN_KB];
-        ptx::tmem_ld32(tmem + lane_base + col_s, reinterpret_cast<uint32_t*>(sv));
-        ptx::tmem_ld32(tmem + lane_base + col_s + 32, reinterpret_cast<uint32_t*>(sv + 32));
+        float sv[32];
+        ptx::tmem_ld32(tmem + lane_base + col_s + 32 * h, reinterpret_cast<uint32_t*>(sv));
         ptx::tmem_wait_ld();
         if (!full_vis) {
 #pragma unroll
-          for (int k = 0; k < DN_KB; ++k) sv[k] = (k % BOX) < vis[k / BOX] ? sv[k] : -INFINITY;
+          for (int k = 0; k < 32; ++k) {
+            const int e = BOX >= 64 ? 0 : k / BOX, kr = BOX >= 64 ? k : k % BOX;
+            sv[k] = kr < vis[e] ? sv[k] : -INFINITY;
+          }
         }
         // P = exp2(s*scale - m) on packed fp32 pairs (FFMA2/FADD2): 3 of every 4 pairs on the
-        // MUFU pipe, 1 of 4 as a polynomial on the FMA pipe; bf16 pairs -> the first 32 TMEM
-        // columns of this S buffer.
-        uint32_t pk[DN_KB / 2];
+        // MUFU pipe, 1 of 4 as a polynomial on the FMA pipe; bf16 pairs -> 16 TMEM columns
+        // of this S buffer (keys 32h.. -> columns 32h..32h+15).
+        uint32_t pk[16];
         float lsum = 0.f;
         auto exps = [&](float m_use) {
           const uint64_t sc2 = ptx::f2pack(p.scale_log2, p.scale_log2), nm2 = ptx::f2pack(-m_use, -m_use);
           uint64_t ls2[2] = {ptx::f2pack(0.f, 0.f), ptx::f2pack(0.f, 0.f)};
 #pragma unroll
-          for (int k = 0; k < DN_KB / 2; ++k) {
+          for (int k = 0; k < 16; ++k) {
             const uint64_t x2 = ptx::ffma2(ptx::f2pack(sv[2 * k], sv[2 * k + 1]), sc2, nm2);
             uint64_t p2;
-            if ((POLY >> (k & 15)) & 1u) {
+            if ((POLY >> k) & 1u) {
               p2 = ptx::exp2_poly2(x2);
             } else {
               float x0, x1;
@@ -497,76 +529,71 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         };
         // Fast path: exponentiate against the running reference m_ref without the block
         // max.  Lazy rescaling keeps m_ref unless the max grows by more than 2^8, i.e. unless
-        // some p > 2^8; the block sum bounds every p, so lsum <= 2^8 proves this block keeps
-        // m_ref and P is exactly what the max-first order computes.  Otherwise (and on a
-        // unit's first block) the warp takes the max-first path below.
-        bool slow = __any_sync(0xffffffffu, row_ok && m_ref == -INFINITY);
+        // some p > 2^8; each half's sum bounds its p, so both halves' sums <= 2^8 (one
+        // barrier reduction over the pair) prove this block keeps m_ref and P is exactly
+        // what the max-first order computes.  Otherwise (and on a unit's first block) the
+        // pair takes the max-first path below.
+        bool slow = __any_sync(0xffffffffu, row_ok && m_ref == -INFINITY);   // same in both halves
         if (!slow) {
           exps(m_ref == -INFINITY ? 0.f : m_ref);   // -inf: a padding row (all scores masked)
-          slow = __any_sync(0xffffffffu, !(lsum <= 256.f));
+          slow = ptx::bar_red_or(pair_bar, 64, !(lsum <= 256.f));
         }
-        if (p.stats != nullptr && lane == 0) {   // diagnostics: blocks per softmax path
+        if (p.stats != nullptr && lane == 0 && h == 0) {   // diagnostics: blocks per softmax path
           stat_add(p, STAT_DENSE_BLOCKS, 1);
           if (slow) stat_add(p, STAT_DENSE_SLOW, 1);
           if (slow && j > 0) stat_add(p, STAT_DENSE_SLOW_LATE, 1);
         }
         if (slow) {
-        float mxv[8];
+          float mxv[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) mxv[i] = sv[i];
+          for (int i = 0; i < 8; ++i) mxv[i] = sv[i];
 #pragma unroll
-        for (int k = 8; k < DN_KB; ++k) mxv[k & 7] = fmaxf(mxv[k & 7], sv[k]);
-        const float mx = fmaxf(fmaxf(fmaxf(mxv[0], mxv[1]), fmaxf(mxv[2], mxv[3])),
-                               fmaxf(fmaxf(mxv[4], mxv[5]), fmaxf(mxv[6], mxv[7])));
-        const float mx2 = mx * p.scale_log2;
-        const bool need = mx2 > m_ref + DN_RESCALE_T;
-        if (j > 0 && __any_sync(0xffffffffu, need)) {
-          if (lane == 0) stat_add(p, STAT_DENSE_RESCALE, 1);
-          // O holds PV up to block j-1: wait for it.  Parity is unambiguous because the
-          // previous completion on this barrier (PV(j-3)) is certified by s_full(j-1) and
-          // PV(j+1) cannot be issued before this block's P.
-          const int pb_ = (j - 1) & 1;
-          ptx::mbar_wait(&o_done[t * 2 + pb_], ((pb_ ? scnt1 : scnt0) - 1) & 1);
-          ptx::tc_fence_after();
-          const float alpha = need ? ptx::ex2(m_ref - mx2) : 1.f;
+          for (int k = 8; k < 32; ++k) mxv[k & 7] = fmaxf(mxv[k & 7], sv[k]);
+          float mx = fmaxf(fmaxf(fmaxf(mxv[0], mxv[1]), fmaxf(mxv[2], mxv[3])),
+                           fmaxf(fmaxf(mxv[4], mxv[5]), fmaxf(mxv[6], mxv[7])));
+          // the row max over both halves: exchange through the pair's smem slots (two
+          // parities, so a slot is rewritten only after the partner has read it)
+          float* xs = reinterpret_cast<float*>(my_x) + (j & 1) * 32;
+          xs[lane] = mx;
+          ptx::bar_sync(pair_bar, 64);
+          mx = fmaxf(mx, reinterpret_cast<const float*>(pa_x)[(j & 1) * 32 + lane]);
+          const float mx2 = mx * p.scale_log2;
+          const bool need = mx2 > m_ref + DN_RESCALE_T;
+          if (j > 0 && __any_sync(0xffffffffu, need)) {
+            if (lane == 0 && h == 0) stat_add(p, STAT_DENSE_RESCALE, 1);
+            // O holds PV up to block j-1: wait for it.  Parity is unambiguous because the
+            // previous completion on this barrier (PV(j-3)) is certified by s_full(j-1) and
+            // PV(j+1) cannot be issued before this block's P.
+            const int pb_ = (j - 1) & 1;
+            ptx::mbar_wait(&o_done[t * 2 + pb_], ((pb_ ? scnt1 : scnt0) - 1) & 1);
+            ptx::tc_fence_after();
+            const float alpha = need ? ptx::ex2(m_ref - mx2) : 1.f;
 #pragma unroll 1
-          for (int c = 0; c < D / 32; ++c) {
-            uint32_t ov[32];
-            ptx::tmem_ld32(tmem + lane_base + col_o + c * 32, ov);
-            ptx::tmem_wait_ld();
+            for (int c = 0; c < DH / 32; ++c) {
+              uint32_t ov[32];
+              ptx::tmem_ld32(tmem + lane_base + col_o + c * 32, ov);
+              ptx::tmem_wait_ld();
 #pragma unroll
-            for (int k = 0; k < 32; ++k) ov[k] = __float_as_uint(__uint_as_float(ov[k]) * alpha);
-            ptx::tmem_st32(tmem + lane_base + col_o + c * 32, ov);
+              for (int k = 0; k < 32; ++k) ov[k] = __float_as_uint(__uint_as_float(ov[k]) * alpha);
+              ptx::tmem_st32(tmem + lane_base + col_o + c * 32, ov);
+            }
           }
-        }
-        if (need) {
-          l *= ptx::ex2(m_ref - mx2);   // m_ref = -inf -> 0
-          m_ref = mx2;
-        }
+          if (need) {
+            l *= ptx::ex2(m_ref - mx2);   // m_ref = -inf -> 0
+            m_ref = mx2;
+          }
           exps(m_ref == -INFINITY ? 0.f : m_ref);
         }
-#pragma unroll
-        for (int c = 0; c < DN_KB / 32; ++c) ptx::tmem_st16(tmem + lane_base + col_s + c * 16, pk + 16 * c);
+        ptx::tmem_st16(tmem + lane_base + col_s + 32 * h, pk);
         l += lsum;
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&p_full[t * 2 + buf]);
-#if BLEND_TRACE_WARPS
-        if (lane == 0 && ui == (int)blockIdx.x && j >= 20 && j < 24) trace_stamp(p, 24 + (j - 20) * 8 + (warp - 4));
-#endif
-#if BLEND_TRACE_BLOCKS
-        if (threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 9 + 2 * j);
-#endif
       }
-      if (threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 4);
+      if (sw == 0 && lane == 0 && ui == (int)blockIdx.x) trace_stamp(p, 4);
 #if BLEND_TRACE_UNITS
-      if (threadIdx.x == 128 && uk < 10) trace_stamp(p, 22 + 4 * uk);
-      const long long cu_lp = clock64();
-      cu_acc[0] += cu_s0 - cu0;
-      cu_acc[1] += cu_lp - cu_s0;
-      cu_acc[4] += nb;
-      cu_acc[5] += 1;
+      if (sw == 0 && lane == 0 && uk < 10) trace_stamp(p, 22 + 4 * uk);
 #endif
       // ---- epilogue: PV of the unit's last block done (MMAs complete in issue order, so
       // this also certifies every earlier PV of the unit)
@@ -575,101 +602,95 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         ptx::mbar_wait(&o_done[t * 2 + lb], ((lb ? scnt1 : scnt0) - 1) & 1);
       }
       ptx::tc_fence_after();
-      if (threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 60);
+      // the row sum over both halves (exchange slot after the two max slots; the second
+      // barrier keeps this warp from overwriting its area before the partner has read it)
+      reinterpret_cast<float*>(my_x)[64 + lane] = l;
+      ptx::bar_sync(pair_bar, 64);
+      l += reinterpret_cast<const float*>(pa_x)[64 + lane];
+      ptx::bar_sync(pair_bar, 64);
       const float m_use = m_ref == -INFINITY ? 0.f : m_ref;
       const float inv = l > 0.f ? 1.f / l : 0.f;
       const float lse2 = l > 0.f ? m_use + log2f(l) : -INFINITY;
-      // O / l leaves through a per-warp smem staging tile (XOR-swizzled 16-B units, no
-      // bank conflicts), so that every global store instruction writes whole row
-      // segments of 4 rows instead of 32 scattered pieces.  Row kinds: 2 = fp32 partial
-      // row, 1 = bf16 output row (DIRECT), 0 = nothing.  A warp whose rows are all bf16
-      // outputs (or nothing) stages 64 columns as bf16 per pass (one 128-B line per row:
-      // every STG.128 writes 4 whole lines); a warp with partial rows stages 32 fp32
-      // columns per pass.
+      // This half's O / l (D/2 columns) leaves through the warp's staging tile (32 rows x
+      // 64 B, XOR-swizzled 16-B units) so that every global store instruction writes 64-B
+      // row segments of 8 rows.  Row kinds: 2 = fp32 partial row, 1 = bf16 output row
+      // (DIRECT), 0 = nothing.  A warp whose rows are all bf16 outputs stages 32 columns
+      // as bf16 per pass; a warp with partial rows 16 fp32 columns.
       {
         const int kind = tgt == PM_DIRECT ? 1 : (tgt >= 0 ? 2 : 0);
-        char* rowp = kind == 1 ? reinterpret_cast<char*>(p.out) + ((int64_t)token * p.hq + head) * D * 2
-                   : kind == 2 ? reinterpret_cast<char*>(p.ws_o + ((int64_t)tgt * p.hq + head) * D) : nullptr;
-        const uint32_t stg = ptx::smem_u32(smem + L.stg + (warp - 4) * 4096);
-        const int k8 = lane & 7;
-        char* rp[8];
-        int rk[8];
+        char* rowp = kind == 1 ? reinterpret_cast<char*>(p.out) + (((int64_t)token * p.hq + head) * D + h * DH) * 2
+                   : kind == 2 ? reinterpret_cast<char*>(p.ws_o + ((int64_t)tgt * p.hq + head) * D + h * DH) : nullptr;
+        const uint32_t stg = ptx::smem_u32(my_x);
+        const int k4 = lane & 3;
+        char* rp[4];
+        int rk[4];
 #pragma unroll
-        for (int s_ = 0; s_ < 8; ++s_) {          // rows s_ * 4 + lane / 8 of this warp, for the copy-out
-          const int rr = s_ * 4 + (lane >> 3);
+        for (int s_ = 0; s_ < 4; ++s_) {          // rows s_ * 8 + lane / 4 of this warp, for the copy-out
+          const int rr = s_ * 8 + (lane >> 2);
           rp[s_] = reinterpret_cast<char*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(rowp), rr));
           rk[s_] = __shfl_sync(0xffffffffu, kind, rr);
         }
+        auto sw64 = [](uint32_t rr, uint32_t c) { return rr * 64u + ((c ^ (rr & 3u)) << 4); };
         const bool all_bf16 = __all_sync(0xffffffffu, kind != 2);
-        // TMEM column loads two chunks at a time (one wait per 64 columns), then through
-        // the staging tile
 #pragma unroll 1
-        for (int hh = 0; hh < D / 64; ++hh) {
-         uint32_t ov2[64];
-         ptx::tmem_ld32(tmem + lane_base + col_o + hh * 64, ov2);
-         ptx::tmem_ld32(tmem + lane_base + col_o + hh * 64 + 32, ov2 + 32);
-         ptx::tmem_wait_ld();
-         if (hh == 0 && threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 62);
-         if (all_bf16) {
+        for (int c32 = 0; c32 < DH / 32; ++c32) {
+          uint32_t ov[32];
+          ptx::tmem_ld32(tmem + lane_base + col_o + c32 * 32, ov);
+          ptx::tmem_wait_ld();
+          if (all_bf16) {            // 32 columns = one 64-B bf16 row segment per pass
 #pragma unroll
-          for (int u8 = 0; u8 < 8; ++u8) {
-            const uint32_t* o8 = ov2 + 8 * u8;
-            ptx::sts128u(stg + ptx::sw128(lane, u8),
-                         ptx::pack_bf16(__uint_as_float(o8[0]) * inv, __uint_as_float(o8[1]) * inv),
-                         ptx::pack_bf16(__uint_as_float(o8[2]) * inv, __uint_as_float(o8[3]) * inv),
-                         ptx::pack_bf16(__uint_as_float(o8[4]) * inv, __uint_as_float(o8[5]) * inv),
-                         ptx::pack_bf16(__uint_as_float(o8[6]) * inv, __uint_as_float(o8[7]) * inv));
+            for (int u4 = 0; u4 < 4; ++u4) {
+              const uint32_t* o8 = ov + 8 * u4;
+              ptx::sts128u(stg + sw64(lane, u4),
+                           ptx::pack_bf16(__uint_as_float(o8[0]) * inv, __uint_as_float(o8[1]) * inv),
+                           ptx::pack_bf16(__uint_as_float(o8[2]) * inv, __uint_as_float(o8[3]) * inv),
+                           ptx::pack_bf16(__uint_as_float(o8[4]) * inv, __uint_as_float(o8[5]) * inv),
+                           ptx::pack_bf16(__uint_as_float(o8[6]) * inv, __uint_as_float(o8[7]) * inv));
+            }
+            __syncwarp();
+            uint4 v[4];
+#pragma unroll
+            for (int s_ = 0; s_ < 4; ++s_) v[s_] = ptx::lds128u(stg + sw64(s_ * 8 + (lane >> 2), k4));
+#pragma unroll
+            for (int s_ = 0; s_ < 4; ++s_)
+              if (rk[s_] == 1) ptx::stg128u(rp[s_] + c32 * 64 + k4 * 16, v[s_]);
+            __syncwarp();   // the staging tile is rewritten by the next pass
+            continue;
           }
-          __syncwarp();
-          uint4 v[8];   // all eight row segments in flight before the first store
 #pragma unroll
-          for (int s_ = 0; s_ < 8; ++s_) v[s_] = ptx::lds128u(stg + ptx::sw128(s_ * 4 + (lane >> 3), k8));
+          for (int cc = 0; cc < 2; ++cc) {   // 16 fp32 columns = one 64-B row segment per pass
+            const uint32_t* o16 = ov + 16 * cc;
 #pragma unroll
-          for (int s_ = 0; s_ < 8; ++s_)
-            if (rk[s_] == 1) ptx::stg128u(rp[s_] + hh * 128 + k8 * 16, v[s_]);
-          __syncwarp();   // the staging tile is rewritten by the next chunk
-          continue;
-         }
+            for (int u4 = 0; u4 < 4; ++u4)
+              ptx::sts128(stg + sw64(lane, u4), __uint_as_float(o16[4 * u4]) * inv,
+                          __uint_as_float(o16[4 * u4 + 1]) * inv, __uint_as_float(o16[4 * u4 + 2]) * inv,
+                          __uint_as_float(o16[4 * u4 + 3]) * inv);
+            __syncwarp();
+            float4 v[4];
 #pragma unroll
-         for (int cc = 0; cc < 2; ++cc) {
-          const int c = 2 * hh + cc;
-          const uint32_t* ov = ov2 + 32 * cc;
+            for (int s_ = 0; s_ < 4; ++s_) v[s_] = ptx::lds128(stg + sw64(s_ * 8 + (lane >> 2), k4));
+            const int c = 2 * c32 + cc;
 #pragma unroll
-          for (int u8 = 0; u8 < 8; ++u8)
-            ptx::sts128(stg + ptx::sw128(lane, u8), __uint_as_float(ov[4 * u8]) * inv,
-                        __uint_as_float(ov[4 * u8 + 1]) * inv, __uint_as_float(ov[4 * u8 + 2]) * inv,
-                        __uint_as_float(ov[4 * u8 + 3]) * inv);
-          __syncwarp();
-          float4 v[8];   // all eight row segments in flight before the first store
-#pragma unroll
-          for (int s_ = 0; s_ < 8; ++s_) v[s_] = ptx::lds128(stg + ptx::sw128(s_ * 4 + (lane >> 3), k8));
-#pragma unroll
-          for (int s_ = 0; s_ < 8; ++s_) {
-            if (rk[s_] == 2)
-              ptx::stg128(rp[s_] + c * 128 + k8 * 16, v[s_]);
-            else if (rk[s_] == 1)
-              ptx::stg64(rp[s_] + c * 64 + k8 * 8, ptx::pack_bf16(v[s_].x, v[s_].y), ptx::pack_bf16(v[s_].z, v[s_].w));
+            for (int s_ = 0; s_ < 4; ++s_) {
+              if (rk[s_] == 2)
+                ptx::stg128(rp[s_] + c * 64 + k4 * 16, v[s_]);
+              else if (rk[s_] == 1)
+                ptx::stg64(rp[s_] + c * 32 + k4 * 8, ptx::pack_bf16(v[s_].x, v[s_].y), ptx::pack_bf16(v[s_].z, v[s_].w));
+            }
+            __syncwarp();   // the staging tile is rewritten by the next pass
           }
-          __syncwarp();   // the staging tile is rewritten by the next chunk
-          if (c == 0 && threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 63);
-         }
         }
       }
-      if (threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 61);
-      if (tgt == PM_DIRECT) p.lse[(int64_t)token * p.hq + head] = lse2 * kLn2;
-      else if (tgt >= 0) p.ws_lse[(int64_t)tgt * p.hq + head] = lse2;
+      if (h == 0) {
+        if (tgt == PM_DIRECT) p.lse[(int64_t)token * p.hq + head] = lse2 * kLn2;
+        else if (tgt >= 0) p.ws_lse[(int64_t)tgt * p.hq + head] = lse2;
+      }
       ptx::tc_fence_before();
-      if (threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 5);
+      if (sw == 0 && lane == 0 && ui == (int)blockIdx.x) trace_stamp(p, 5);
 #if BLEND_TRACE_UNITS
-      if (threadIdx.x == 128 && uk < 10) trace_stamp(p, 23 + 4 * uk);
-      cu_prev_end = clock64();
-      cu_acc[2] += cu_prev_end - cu_lp;
+      if (sw == 0 && lane == 0 && uk < 10) trace_stamp(p, 23 + 4 * uk);
 #endif
     }
-#if BLEND_TRACE_UNITS
-    if (threadIdx.x == 128 && p.trace != nullptr)
-      for (int i = 0; i < 6; ++i) p.trace[(size_t)blockIdx.x * 64 + 40 + i] = (unsigned long long)cu_acc[i];
-#endif
   }
   __syncwarp();       // lane 0 of the producer / MMA warps rejoins its warp before the CTA barrier
   ptx::tc_fence_before();
