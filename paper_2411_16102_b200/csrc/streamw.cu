@@ -475,7 +475,10 @@ static cudaError_t launch_streamw_d(const AttnParams& p, int64_t n_cache_pages, 
   e = set_smem_once((const void*)streamw_kernel<D>, smem);
   if (e != cudaSuccess) return e;
   const int warps = (p.n_units + SW_WARPS - 1) / SW_WARPS;
-  const int grid = warps < num_sms_cached() ? warps : num_sms_cached();
+  int grid = warps < num_sms_cached() ? warps : num_sms_cached();
+#ifdef SW_GRID_CAP
+  if (grid > SW_GRID_CAP) grid = SW_GRID_CAP;   // diagnostics: bandwidth of the pass on fewer SMs
+#endif
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(SW_THREADS);
