@@ -227,7 +227,8 @@ def run_reference(args):
     value = tot_tok / tot_t
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True,
+            "scaling": "weak" if args.weak else "strong",   # mirrors this repo's arm for the same flags
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": w.name, "requests": w.n_req, "query_tokens": int(w.sum_q),
                        "heads": f"{w.num_q_heads}/{w.num_kv_heads}x{w.head_dim}", "page_size": w.page_size,
