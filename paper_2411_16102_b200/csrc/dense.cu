@@ -358,7 +358,9 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
     const uint32_t col_o = 256 + t * D;
     uint32_t sb = 0;                                  // blocks of this tile processed so far
 #if BLEND_TRACE_UNITS
-    long long cu_acc[6] = {0, 0, 0, 0, 0, 0};         // clock64 sums: start->S0, S0->last P, epilogue, gap; blocks; units
+    long long ph_acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};   // per fast block: two-tile [4], single-tile [4], counts [2]
+    long long cu_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // clock64 sums: start->S0, S0->last P, epilogue, gap; blocks; units;
+                                                      // single-tile units: S0->last P, blocks
     long long cu_prev_end = 0;
 #endif
     uint32_t scnt0 = 0, scnt1 = 0;                    // s_full completions consumed per S buffer (registers)
@@ -421,7 +423,13 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
           vis[i] = v;
           full_vis = full_vis && (v == BOX);
         }
+#if BLEND_TRACE_UNITS
+        const long long ph0 = clock64();
+#endif
         ptx::mbar_wait(&s_full[t * 2 + buf], (buf ? scnt1++ : scnt0++) & 1);   // per-buffer completion count
+#if BLEND_TRACE_UNITS
+        const long long ph1 = clock64();
+#endif
         ptx::tc_fence_after();
 #if BLEND_TRACE_UNITS
         if (threadIdx.x == 128 && uk < 10 && j == 0) trace_stamp(p, 21 + 4 * uk);
@@ -462,6 +470,10 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         ptx::tmem_ld32(tmem + lane_base + col_s, reinterpret_cast<uint32_t*>(sv));
         ptx::tmem_ld32(tmem + lane_base + col_s + 32, reinterpret_cast<uint32_t*>(sv + 32));
         ptx::tmem_wait_ld();
+#if BLEND_TRACE_UNITS
+        const long long ph2 = clock64();
+        long long ph3 = ph2;
+#endif
         if (!full_vis) {
 #pragma unroll
           for (int k = 0; k < DN_KB; ++k) sv[k] = (k % BOX) < vis[k / BOX] ? sv[k] : -INFINITY;
@@ -503,6 +515,9 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         bool slow = __any_sync(0xffffffffu, row_ok && m_ref == -INFINITY);
         if (!slow) {
           exps(m_ref == -INFINITY ? 0.f : m_ref);   // -inf: a padding row (all scores masked)
+#if BLEND_TRACE_UNITS
+          ph3 = clock64();
+#endif
           slow = __any_sync(0xffffffffu, !(lsum <= 256.f));
         }
         if (p.stats != nullptr && lane == 0) {   // diagnostics: blocks per softmax path
@@ -552,6 +567,17 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&p_full[t * 2 + buf]);
+#if BLEND_TRACE_UNITS
+        if (threadIdx.x == 128 && !slow) {
+          const long long ph5 = clock64();
+          const int k0 = u.n_rows <= 128 ? 52 : 48;   // [single-tile | two-tile]: s wait, ld, exps, st+arrive
+          ph_acc[k0 - 48] += ph1 - ph0;
+          ph_acc[k0 - 47] += ph2 - ph1;
+          ph_acc[k0 - 46] += ph3 - ph2;
+          ph_acc[k0 - 45] += ph5 - ph3;
+          ph_acc[8 + (k0 == 52)] += 1;
+        }
+#endif
 #if BLEND_TRACE_WARPS
         if (lane == 0 && ui == (int)blockIdx.x && j >= 20 && j < 24) trace_stamp(p, 24 + (j - 20) * 8 + (warp - 4));
 #endif
@@ -566,6 +592,10 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       cu_acc[0] += cu_s0 - cu0;
       cu_acc[1] += cu_lp - cu_s0;
       cu_acc[4] += nb;
+      if (u.n_rows <= 128) {
+        cu_acc[6] += cu_lp - cu_s0;
+        cu_acc[7] += nb;
+      }
       cu_acc[5] += 1;
 #endif
       // ---- epilogue: PV of the unit's last block done (MMAs complete in issue order, so
@@ -667,8 +697,10 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
 #endif
     }
 #if BLEND_TRACE_UNITS
-    if (threadIdx.x == 128 && p.trace != nullptr)
-      for (int i = 0; i < 6; ++i) p.trace[(size_t)blockIdx.x * 64 + 40 + i] = (unsigned long long)cu_acc[i];
+    if (threadIdx.x == 128 && p.trace != nullptr) {
+      for (int i = 0; i < 8; ++i) p.trace[(size_t)blockIdx.x * 64 + 40 + i] = (unsigned long long)cu_acc[i];
+      for (int i = 0; i < 10; ++i) p.trace[(size_t)blockIdx.x * 64 + 48 + i] = (unsigned long long)ph_acc[i];
+    }
 #endif
   }
   __syncwarp();       // lane 0 of the producer / MMA warps rejoins its warp before the CTA barrier

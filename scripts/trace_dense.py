@@ -69,6 +69,7 @@ for k in list(range(7)) + [60, 62, 63, 61] + list(range(8, 20)):
 if tall[:148, 45].max() > 0:
     # BLEND_TRACE_UNITS: clock64 sums over ALL units of tile A per CTA (slots 40..45)
     a = tall[:148, 40:46].astype(np.float64)
+    keep = a[:, 5] > 0
     a = a[a[:, 5] > 0]
     units, blocks = a[:, 5], a[:, 4]
     tot = a[:, 0:4].sum(1)
@@ -77,9 +78,15 @@ if tall[:148, 45].max() > 0:
     for i, nm in enumerate(["start -> first S", "first S -> last P", "last P -> epilogue end", "epilogue end -> next start"]):
         print(f"  {nm:28s} {np.median(a[:, i] / units):9.0f} cycles / unit  ({np.median(a[:, i] / tot) * 100:5.1f} %)")
     print(f"  blocks: {np.median(a[:, 1] / np.maximum(blocks - units, 1)):.0f} cycles per block after the first")
-if tall[:148, 55].max() > 0:
-    ph = tall[:148, 50:56].astype(np.float64)
-    ph = ph[ph[:, 5] > 0]
-    print("softmax phases per fast block (tile A, clock64, median over CTAs):")
-    for i, nm in enumerate(["s_full wait", "S ld (+zeroing)", "mask + exps + sums", "PV(j-1) wait", "P st + fence + arrive"]):
-        print(f"  {nm:24s} {np.median(ph[:, i] / ph[:, 5]):8.0f}")
+    b = tall[:148, 46:48].astype(np.float64)[tall[:148, 45] > 0]
+    if b[:, 1].sum() > 0:
+        two_c, two_b = a[:, 1] - b[:, 0], blocks - b[:, 1]
+        print(f"  single-tile units: {np.median(b[:, 1]):.0f} blocks per CTA at {np.median(b[:, 0] / np.maximum(b[:, 1], 1)):.0f} "
+              f"cycles per block; two-tile units: {np.median(two_b):.0f} blocks at {np.median(two_c / np.maximum(two_b, 1)):.0f}")
+if tall[:148, 56].max() > 0:
+    ph = tall[:148, 48:58].astype(np.float64)
+    ph = ph[ph[:, 8] > 0]
+    print("softmax phases per fast block (tile A, clock64 cycles, median over CTAs): S wait, S ld, exps, P st + arrive")
+    for nm, o, c in (("two-tile units", 0, 8), ("single-tile units", 4, 9)):
+        n = np.maximum(ph[:, c], 1)
+        print(f"  {nm:18s} " + "  ".join(f"{np.median(ph[:, o + i] / n):7.0f}" for i in range(4)))
