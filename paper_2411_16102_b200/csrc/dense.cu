@@ -62,7 +62,7 @@ constexpr uint32_t DN_TMEM_COLS = 512;
 constexpr float DN_RESCALE_T = 8.0f;     // lazy-rescale threshold (log2 units)
 
 struct DenseSmem {
-  uint32_t q0, q1, stage0, stage_stride, bar, stg, total;
+  uint32_t q0, q1, k0, v0, slot, bar, stg, total;
   int nstage;
 };
 
@@ -71,10 +71,11 @@ __host__ __device__ inline DenseSmem dense_layout(int D) {
   const int CH = D / 64;
   L.q0 = 0;
   L.q1 = CH * DN_QCHUNK;
-  L.stage0 = 2 * CH * DN_QCHUNK;
-  L.stage_stride = 2 * CH * DN_KCHUNK;   // K chunks then V chunks
+  L.slot = CH * DN_KCHUNK;               // one 64-key K (or V) block
   L.nstage = D == 128 ? DN_NSTAGE128 : 8;
-  L.bar = L.stage0 + L.nstage * L.stage_stride;
+  L.k0 = 2 * CH * DN_QCHUNK;             // K ring, then V ring (a K slot frees at QK, a V slot at PV)
+  L.v0 = L.k0 + L.nstage * L.slot;
+  L.bar = L.v0 + L.nstage * L.slot;
   L.stg = L.bar + 512;                    // epilogue staging: per softmax warp 32 rows x 128 B
   L.total = L.stg + 8 * 4096;
   return L;
@@ -102,14 +103,16 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
   const DenseSmem L = dense_layout(D);
   const int NS = L.nstage;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar);
-  uint64_t* kv_full = bars;            // [NS <= 8]
-  uint64_t* kv_empty = bars + 8;       // [NS]
-  uint64_t* s_full = bars + 16;        // [tile][buffer]
-  uint64_t* p_full = bars + 20;        // [tile][buffer]
-  uint64_t* o_done = bars + 24;        // [tile][buffer]: PV of a block that used this S buffer
-  uint64_t* q_full = bars + 28;
-  uint64_t* q_empty = bars + 29;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 30);
+  uint64_t* k_full = bars;             // [NS <= 8]
+  uint64_t* k_empty = bars + 8;        // [NS]: every QK that reads the K slot issued (and done)
+  uint64_t* v_full = bars + 16;        // [NS]
+  uint64_t* v_empty = bars + 24;       // [NS]: every PV that reads the V slot done
+  uint64_t* s_full = bars + 32;        // [tile][buffer]
+  uint64_t* p_full = bars + 36;        // [tile][buffer]
+  uint64_t* o_done = bars + 40;        // [tile][buffer]: PV of a block that used this S buffer
+  uint64_t* q_full = bars + 44;
+  uint64_t* q_empty = bars + 45;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 46);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) trace_stamp(p, 0);
@@ -125,8 +128,10 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
   ptx::pdl_launch_dependents();   // the streaming pass may start on SMs this grid leaves free
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
-      ptx::mbar_init(&kv_full[s], 1);
-      ptx::mbar_init(&kv_empty[s], 1);
+      ptx::mbar_init(&k_full[s], 1);
+      ptx::mbar_init(&k_empty[s], 1);
+      ptx::mbar_init(&v_full[s], 1);
+      ptx::mbar_init(&v_empty[s], 1);
     }
     for (int i = 0; i < 4; ++i) {
       ptx::mbar_init(&s_full[i], 1);
@@ -151,9 +156,12 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
   if (warp < 4) {
   ptx::setmaxnreg_dec<56>();
   if (warp == 0) {
-    // ===================== TMA producer: 64-key K/V blocks into the stage ring =====================
-    // The entries of the next block (and the next unit's header) are loaded one step
-    // ahead, so a freed stage is refilled without waiting on dependent global loads.
+    // ===================== TMA producer: 64-key K blocks and V blocks into their rings =====================
+    // The CTA's blocks form one stream b = 0, 1, ...; the loop issues K(b) and then V(b-1),
+    // so a K block (needed by the next QK) never waits behind a V slot (freed only by the
+    // PV two blocks later).  The entries of the next block (and the next unit's header)
+    // are loaded one step ahead, so a freed slot is refilled without waiting on dependent
+    // global loads.
     if (lane == 0) {
       ptx::tma_prefetch_desc(&tmk);
       ptx::tma_prefetch_desc(&tmv);
@@ -162,6 +170,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       int uk = 0, ui = snake_unit(0);
       Unit u = ui < p.n_units ? p.units[ui] : Unit{};
       int4 cur[EPB];
+      int32_t yprev[EPB];   // TMA rows of block kit-1 (its V is issued after K(kit))
       auto load_block = [&](const Unit& un, int j) {
 #pragma unroll
         for (int i = 0; i < EPB; ++i) {
@@ -172,6 +181,16 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
           if (pad) cur[i].w = 0;
         }
       };
+      auto issue_v = [&](uint32_t b) {
+        const uint32_t s = b % NS, ph = (b / NS) & 1;
+        ptx::mbar_wait(&v_empty[s], ph ^ 1);
+        uint8_t* vst = smem + L.v0 + s * L.slot;
+        ptx::mbar_arrive_expect_tx(&v_full[s], (uint32_t)(CH * DN_KCHUNK));
+#pragma unroll
+        for (int i = 0; i < EPB; ++i)
+#pragma unroll
+          for (int c = 0; c < CH; ++c) ptx::tma_load_2d(vst + c * DN_KCHUNK + i * BOX * 128, &tmv, &v_full[s], c * 64, yprev[i]);
+      };
       if (ui < p.n_units) load_block(u, 0);
       while (ui < p.n_units) {
         const int nb = (u.entry_end - u.entry_begin + EPB - 1) / EPB;
@@ -179,26 +198,27 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         const Unit un = ui_next < p.n_units ? p.units[ui_next] : Unit{};
         for (int j = 0; j < nb; ++j, ++kit) {
           const uint32_t s = kit % NS, ph = (kit / NS) & 1;
-          ptx::mbar_wait(&kv_empty[s], ph ^ 1);
-          uint8_t* kst = smem + L.stage0 + s * L.stage_stride;
-          uint8_t* vst = kst + CH * DN_KCHUNK;
+          ptx::mbar_wait(&k_empty[s], ph ^ 1);
+          uint8_t* kst = smem + L.k0 + s * L.slot;
           if (kit == 0) trace_stamp(p, 3);
-          ptx::mbar_arrive_expect_tx(&kv_full[s], 2u * CH * DN_KCHUNK);
+          ptx::mbar_arrive_expect_tx(&k_full[s], (uint32_t)(CH * DN_KCHUNK));
+          int32_t y[EPB];
 #pragma unroll
           for (int i = 0; i < EPB; ++i) {
-            const int32_t y = (cur[i].x * p.hkv + u.kvh) * p.ps + cur[i].y;   // {page, row_off, pos0, count}
+            y[i] = (cur[i].x * p.hkv + u.kvh) * p.ps + cur[i].y;   // {page, row_off, pos0, count}
 #pragma unroll
-            for (int c = 0; c < CH; ++c) {
-              ptx::tma_load_2d(kst + c * DN_KCHUNK + i * BOX * 128, &tmk, &kv_full[s], c * 64, y);
-              ptx::tma_load_2d(vst + c * DN_KCHUNK + i * BOX * 128, &tmv, &kv_full[s], c * 64, y);
-            }
+            for (int c = 0; c < CH; ++c) ptx::tma_load_2d(kst + c * DN_KCHUNK + i * BOX * 128, &tmk, &k_full[s], c * 64, y[i]);
           }
+          if (kit > 0) issue_v(kit - 1);
+#pragma unroll
+          for (int i = 0; i < EPB; ++i) yprev[i] = y[i];
           if (j + 1 < nb) load_block(u, j + 1);
           else if (ui_next < p.n_units) load_block(un, 0);
         }
         ui = ui_next;
         u = un;
       }
+      if (kit > 0) issue_v(kit - 1);
     }
   } else if (warp == 3) {
     // ===================== Q loader: next unit's rows as soon as its last QK is issued =====
@@ -291,11 +311,11 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       const uint64_t qd0 = ptx::umma_desc_sw128(ptx::smem_u32(smem + L.q0), 16, 1024);
       const uint32_t q_lo0 = (uint32_t)qd0, q_hi = (uint32_t)(qd0 >> 32);
       const uint32_t q_lo1 = (uint32_t)ptx::umma_desc_sw128(ptx::smem_u32(smem + L.q1), 16, 1024);
-      const uint64_t kd0 = ptx::umma_desc_sw128(ptx::smem_u32(smem + L.stage0), 16, 1024);
+      const uint64_t kd0 = ptx::umma_desc_sw128(ptx::smem_u32(smem + L.k0), 16, 1024);
       const uint32_t k_lo0 = (uint32_t)kd0, k_hi = (uint32_t)(kd0 >> 32);
-      const uint64_t vd0 = ptx::umma_desc_sw128(ptx::smem_u32(smem + L.stage0 + CH * DN_KCHUNK), DN_KCHUNK, 1024);
+      const uint64_t vd0 = ptx::umma_desc_sw128(ptx::smem_u32(smem + L.v0), DN_KCHUNK, 1024);
       const uint32_t v_lo0 = (uint32_t)vd0, v_hi = (uint32_t)(vd0 >> 32);
-      const uint32_t stage_lo = L.stage_stride >> 4;
+      const uint32_t stage_lo = L.slot >> 4;
       const uint32_t leader = ptx::elect_one();
       uint32_t kit = 0, gu = 0;
       uint32_t pbits = 0;               // parity of the next p_full[tile][buffer] completion (bit pi)
@@ -303,8 +323,12 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         const Unit u = p.units[ui];
         const int nb = (u.entry_end - u.entry_begin + EPB - 1) / EPB;
         const int ntile = u.n_rows > 128 ? 2 : 1;
-        auto wait_kv = [&](int j) {
-          ptx::mbar_wait(&kv_full[(kit + j) % NS], ((kit + j) / NS) & 1);
+        auto wait_k = [&](int j) {
+          ptx::mbar_wait(&k_full[(kit + j) % NS], ((kit + j) / NS) & 1);
+          ptx::tc_fence_after();
+        };
+        auto wait_v = [&](int j) {
+          ptx::mbar_wait(&v_full[(kit + j) % NS], ((kit + j) / NS) & 1);
           ptx::tc_fence_after();
         };
         auto issue_qk = [&](int t, int j) {
@@ -321,13 +345,15 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         ptx::tc_fence_after();
         if (gu == 0 && lane == 0) trace_stamp(p, 2);
         for (int j = 0; j < 2 && j < nb; ++j) {
-          wait_kv(j);
+          wait_k(j);
           for (int t = 0; t < ntile; ++t) issue_qk(t, j);
+          ptx::umma_commit_if(leader, &k_empty[(kit + j) % NS]);   // every QK(j) issued
         }
         if (nb <= 2) ptx::umma_commit_if(leader, q_empty);   // every QK of the unit issued: Q may be reloaded
         for (int j = 0; j < nb; ++j) {
           const uint32_t vlo = v_lo0 + ((kit + j) % NS) * stage_lo;
-          if (j + 2 < nb) wait_kv(j + 2);
+          wait_v(j);
+          if (j + 2 < nb) wait_k(j + 2);
           for (int t = 0; t < ntile; ++t) {
             const int pi = t * 2 + (j & 1);
             ptx::mbar_wait(&p_full[pi], (pbits >> pi) & 1);
@@ -342,7 +368,8 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
             if (j + 2 < nb) issue_qk(t, j + 2);
           }
           if (j + 3 == nb) ptx::umma_commit_if(leader, q_empty);   // QK(nb-1) of every tile issued
-          ptx::umma_commit_if(leader, &kv_empty[(kit + j) % NS]);
+          if (j + 2 < nb) ptx::umma_commit_if(leader, &k_empty[(kit + j + 2) % NS]);   // every QK(j+2) issued
+          ptx::umma_commit_if(leader, &v_empty[(kit + j) % NS]);   // every PV(j) issued
         }
         kit += nb;
         ++gu;
@@ -444,7 +471,8 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
 #pragma unroll
           for (int i = 0; i < EPB; ++i) part = part || ecur[i].y < BOX;
           if (part) {
-            uint8_t* vst = smem + L.stage0 + (sb % NS) * L.stage_stride + CH * DN_KCHUNK;
+            ptx::mbar_wait(&v_full[sb % NS], (sb / NS) & 1);   // V(j) has landed (K and V arrive separately)
+            uint8_t* vst = smem + L.v0 + (sb % NS) * L.slot;
 #pragma unroll
             for (int i = 0; i < EPB; ++i) {
               const int nz = BOX - ecur[i].y;
