@@ -22,6 +22,7 @@ cudaError_t launch_generic(const AttnParams& p, cudaStream_t st);
 cudaError_t launch_merge(const AttnParams& p, cudaStream_t st, bool pdl);
 cudaError_t launch_streamw(const AttnParams& p, int64_t n_cache_pages, cudaStream_t st, bool overlap);
 cudaError_t launch_dense(const AttnParams& p, int64_t n_cache_pages, cudaStream_t st);
+cudaError_t launch_dense_ks(const AttnParams& p, int64_t n_cache_pages, cudaStream_t st, bool overlap);
 }  // namespace blend
 
 // Diagnostics (blend_internal_set_trace / _set_stats): per-thread so that callers
@@ -160,6 +161,24 @@ extern "C" int blend_attention(const blend_attn_args* a, void* stream) {
   if (generic || a->path == BLEND_PATH_NO_TCGEN05) e = launch_generic(pd, st);
   else e = launch_dense(pd, a->n_cache_pages, st);
   if (e != cudaSuccess) return cuda_fail(e);
+  // key-split units (<= 128 rows): dense_ks.cu, after the two-tile grid when serialised,
+  // after the streaming grid (its PDL dependent) when overlapped; generic paths run them
+  // with the other units
+  AttnParams pk = p;
+  pk.units = (const Unit*)(base + pl.off[SEC_DENSE_KS]);
+  pk.n_units = (int32_t)pl.count[SEC_DENSE_KS];
+  pk.dqtok = (const int32_t*)(base + pl.off[SEC_DENSE_KS_QTOK]);
+  pk.trace = nullptr;
+  pk.sched = nullptr;
+  const bool ks_tc = pk.n_units > 0 && !generic && a->path != BLEND_PATH_NO_TCGEN05;
+  if (pk.n_units > 0 && !ks_tc) {
+    e = launch_generic(pk, st);
+    if (e != cudaSuccess) return cuda_fail(e);
+  }
+  if (ks_tc && !overlap) {
+    e = launch_dense_ks(pk, a->n_cache_pages, st, false);
+    if (e != cudaSuccess) return cuda_fail(e);
+  }
 
   if (a->events[1]) cudaEventRecord((cudaEvent_t)a->events[1], st);
   AttnParams ps_ = p;
@@ -170,6 +189,10 @@ extern "C" int blend_attention(const blend_attn_args* a, void* stream) {
   if (generic) e = launch_generic(ps_, st);
   else e = launch_streamw(ps_, a->n_cache_pages, st, overlap);
   if (e != cudaSuccess) return cuda_fail(e);
+  if (ks_tc && overlap) {
+    e = launch_dense_ks(pk, a->n_cache_pages, st, true);
+    if (e != cudaSuccess) return cuda_fail(e);
+  }
 
   if (a->events[2]) cudaEventRecord((cudaEvent_t)a->events[2], st);
   AttnParams pm = p;

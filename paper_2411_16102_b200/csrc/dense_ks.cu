@@ -1,35 +1,19 @@
-// dense.cu — the dense pass on the 5th-gen tensor cores (tcgen05 + TMEM + TMA).
+// dense_ks.cu — the dense pass for key-split units (tcgen05 + TMEM + TMA).
 //
-// Work units with many rows per kv head — a SEPARATE shared-prefix node attended
-// once by all the SMALL requests under it (PAPER §5 P:11 "exactly-once computation
-// of shared prefixes"; §7.2 P:248-251 cascade reuse of the shared KV access), or a
-// BIG request (chunked prefill) — are dense contractions: up to 256 query
-// rows (tokens x grouped q heads) against 64-key blocks of the node's pages.
-//
-// One persistent CTA per SM, warp-specialised, two 128-row Q tiles (A, B) that
-// share every K/V block ("ping-pong": the tensor pipe works on one tile while the
-// other tile's softmax runs):
-//   warp 0       TMA producer: 64-key K/V blocks (page entries, 128B swizzle) into a
-//                4-stage smem ring
-//   warp 1       MMA issuer (whole warp, one elected lane issues): S_t = Q_t K^T (UMMA
-//                128x64x16, K-major A/B) into one of two TMEM S buffers per tile;
-//                O_t += P_t V with P_t read from TMEM (aliasing its S buffer) and V
-//                MN-major from smem; tcgen05.commit -> mbarriers
-//   warp 2       TMEM allocator (512 columns: S_A0 S_A1 | S_B0 S_B1 | O_A | O_B)
-//   warp 3       Q loader: the next unit's Q tiles as soon as the current unit's last
-//                QK has been issued — 3-D TMA boxes {64, g, 128/g} when the unit's
-//                tokens are consecutive rows of q, one box per token otherwise,
-//                cp.async row gathers when g does not divide 128
-//   warps 4..7   softmax / epilogue of tile A, warps 8..11 of tile B: thread =
-//                query row = TMEM lane; tcgen05.ld the S row, per-row causal mask,
-//                log2-domain online softmax with lazy O rescaling (only when the
-//                running max grows by > 2^8; blocks whose exponentials sum to <= 2^8
-//                against the running reference skip the block max), exp2 3/4 on
-//                MUFU and 1/4 as an FMA-pipe polynomial, P -> bf16 -> tcgen05.st,
-//                final O / l through a per-warp smem staging tile with coalesced
-//                row-segment stores (bf16 output rows or fp32 partial rows).
-// MMAs of one thread execute in issue order, so QK_t(j+2) (which overwrites the S
-// buffer holding P_t(j)) is issued right after PV_t(j) without a further barrier.
+// A dense unit with at most 128 query rows (a short prefill chunk, or a chunk's last
+// rows) fills one 128-row Q tile; run like the two-tile units of dense.cu it would
+// leave the second tile of the CTA idle and its tensor / softmax pipeline without a
+// ping-pong partner (measured: ~1,670 cycles per 64-key block against ~1,880 for a block
+// of two tiles, i.e. 86 % of the time for half the work).  Here both tiles serve the
+// unit's rows: tile t takes the 64-key blocks j = t (mod 2) — both read the one Q tile —
+// and the two partial results are merged by log-sum-exp at the epilogue (the
+// same identity the LSE-merge pass uses):
+//   O = (2^(mA-m) O_A + 2^(mB-m) O_B) / (2^(mA-m) lA + 2^(mB-m) lB),  m = max(mA, mB).
+// K and V have separate rings (a K slot frees as soon as its QK is done), so the QK of
+// a tile's next-but-one block (4 blocks ahead) never waits for its K.  The kernel is a
+// separate launch (a PDL dependent of the streaming grid) so that dense.cu's two-tile
+// kernel keeps its own code generation.  Warp roles, TMEM map and the softmax are those
+// of dense.cu.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <math.h>
@@ -40,6 +24,7 @@
 #include "ptx.cuh"
 
 namespace blend {
+namespace ks {
 
 #ifndef DN_NSTAGE128
 #define DN_NSTAGE128 4     // K/V ring stages at D = 128 (64 keys each)
@@ -62,7 +47,7 @@ constexpr uint32_t DN_TMEM_COLS = 512;
 constexpr float DN_RESCALE_T = 8.0f;     // lazy-rescale threshold (log2 units)
 
 struct DenseSmem {
-  uint32_t q0, q1, stage0, stage_stride, bar, stg, total;
+  uint32_t q0, q1, k0, v0, slot, bar, stg, total;
   int nstage;
 };
 
@@ -71,10 +56,11 @@ __host__ __device__ inline DenseSmem dense_layout(int D) {
   const int CH = D / 64;
   L.q0 = 0;
   L.q1 = CH * DN_QCHUNK;
-  L.stage0 = 2 * CH * DN_QCHUNK;
-  L.stage_stride = 2 * CH * DN_KCHUNK;   // K chunks then V chunks
+  L.slot = CH * DN_KCHUNK;               // one 64-key K (or V) block
   L.nstage = D == 128 ? DN_NSTAGE128 : 8;
-  L.bar = L.stage0 + L.nstage * L.stage_stride;
+  L.k0 = 2 * CH * DN_QCHUNK;             // K ring, then V ring (a K slot frees at QK, a V slot at PV)
+  L.v0 = L.k0 + L.nstage * L.slot;
+  L.bar = L.v0 + L.nstage * L.slot;
   L.stg = L.bar + 512;                    // epilogue staging: per softmax warp 32 rows x 128 B
   L.total = L.stg + 8 * 4096;
   return L;
@@ -92,7 +78,7 @@ __device__ __forceinline__ int snake_unit(int k) {
 // POLY: bit k set -> pair k (of 16 per 32-key chunk) takes the FMA-pipe polynomial exp2
 template <int D, int BOX, uint32_t POLY = 0x8888u>
 __global__ void __launch_bounds__(DN_THREADS, 1)
-    dense_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
+    dense_ks_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
                  const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmq1,
                  AttnParams p) {
   constexpr int CH = D / 64;
@@ -102,31 +88,26 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
   const DenseSmem L = dense_layout(D);
   const int NS = L.nstage;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar);
-  uint64_t* kv_full = bars;            // [NS <= 8]
-  uint64_t* kv_empty = bars + 8;       // [NS]
-  uint64_t* s_full = bars + 16;        // [tile][buffer]
-  uint64_t* p_full = bars + 20;        // [tile][buffer]
-  uint64_t* o_done = bars + 24;        // [tile][buffer]: PV of a block that used this S buffer
-  uint64_t* q_full = bars + 28;
-  uint64_t* q_empty = bars + 29;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 30);
+  uint64_t* k_full = bars;             // [NS <= 8]
+  uint64_t* k_empty = bars + 8;        // [NS]: every QK that reads the K slot issued (and done)
+  uint64_t* v_full = bars + 16;        // [NS]
+  uint64_t* v_empty = bars + 24;       // [NS]: every PV that reads the V slot done
+  uint64_t* s_full = bars + 32;        // [tile][buffer]
+  uint64_t* p_full = bars + 36;        // [tile][buffer]
+  uint64_t* o_done = bars + 40;        // [tile][buffer]: PV of a block that used this S buffer
+  uint64_t* q_full = bars + 44;
+  uint64_t* q_empty = bars + 45;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 46);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) trace_stamp(p, 0);
-  if (p.sched != nullptr && blockIdx.x == 0) {
-    // reset the streaming pass's unit counter before this CTA's launch trigger: the
-    // dependent (streaming) grid cannot start before every CTA of this grid has triggered
-    if (threadIdx.x == 0) {
-      if (atomicExch(p.sched, 0) == 0x7fffffff) __trap();   // consumes the result: the exchange has completed
-      __threadfence();
-    }
-    __syncthreads();
-  }
-  ptx::pdl_launch_dependents();   // the streaming pass may start on SMs this grid leaves free
+  ptx::pdl_launch_dependents();   // the merge grid may be scheduled (it waits for this grid first)
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
-      ptx::mbar_init(&kv_full[s], 1);
-      ptx::mbar_init(&kv_empty[s], 1);
+      ptx::mbar_init(&k_full[s], 1);
+      ptx::mbar_init(&k_empty[s], 1);
+      ptx::mbar_init(&v_full[s], 1);
+      ptx::mbar_init(&v_empty[s], 1);
     }
     for (int i = 0; i < 4; ++i) {
       ptx::mbar_init(&s_full[i], 1);
@@ -151,9 +132,12 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
   if (warp < 4) {
   ptx::setmaxnreg_dec<56>();
   if (warp == 0) {
-    // ===================== TMA producer: 64-key K/V blocks into the stage ring =====================
-    // The entries of the next block (and the next unit's header) are loaded one step
-    // ahead, so a freed stage is refilled without waiting on dependent global loads.
+    // ===================== TMA producer: 64-key K blocks and V blocks into their rings =====================
+    // The CTA's blocks form one stream b = 0, 1, ...; the loop issues K(b) and then V(b-1),
+    // so a K block (needed by the next QK) never waits behind a V slot (freed only by the
+    // PV two blocks later).  The entries of the next block (and the next unit's header)
+    // are loaded one step ahead, so a freed slot is refilled without waiting on dependent
+    // global loads.
     if (lane == 0) {
       ptx::tma_prefetch_desc(&tmk);
       ptx::tma_prefetch_desc(&tmv);
@@ -162,6 +146,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       int uk = 0, ui = snake_unit(0);
       Unit u = ui < p.n_units ? p.units[ui] : Unit{};
       int4 cur[EPB];
+      int32_t yprev[EPB];   // TMA rows of block kit-1 (its V is issued after K(kit))
       auto load_block = [&](const Unit& un, int j) {
 #pragma unroll
         for (int i = 0; i < EPB; ++i) {
@@ -172,6 +157,16 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
           if (pad) cur[i].w = 0;
         }
       };
+      auto issue_v = [&](uint32_t b) {
+        const uint32_t s = b % NS, ph = (b / NS) & 1;
+        ptx::mbar_wait(&v_empty[s], ph ^ 1);
+        uint8_t* vst = smem + L.v0 + s * L.slot;
+        ptx::mbar_arrive_expect_tx(&v_full[s], (uint32_t)(CH * DN_KCHUNK));
+#pragma unroll
+        for (int i = 0; i < EPB; ++i)
+#pragma unroll
+          for (int c = 0; c < CH; ++c) ptx::tma_load_2d(vst + c * DN_KCHUNK + i * BOX * 128, &tmv, &v_full[s], c * 64, yprev[i]);
+      };
       if (ui < p.n_units) load_block(u, 0);
       while (ui < p.n_units) {
         const int nb = (u.entry_end - u.entry_begin + EPB - 1) / EPB;
@@ -179,26 +174,27 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         const Unit un = ui_next < p.n_units ? p.units[ui_next] : Unit{};
         for (int j = 0; j < nb; ++j, ++kit) {
           const uint32_t s = kit % NS, ph = (kit / NS) & 1;
-          ptx::mbar_wait(&kv_empty[s], ph ^ 1);
-          uint8_t* kst = smem + L.stage0 + s * L.stage_stride;
-          uint8_t* vst = kst + CH * DN_KCHUNK;
+          ptx::mbar_wait(&k_empty[s], ph ^ 1);
+          uint8_t* kst = smem + L.k0 + s * L.slot;
           if (kit == 0) trace_stamp(p, 3);
-          ptx::mbar_arrive_expect_tx(&kv_full[s], 2u * CH * DN_KCHUNK);
+          ptx::mbar_arrive_expect_tx(&k_full[s], (uint32_t)(CH * DN_KCHUNK));
+          int32_t y[EPB];
 #pragma unroll
           for (int i = 0; i < EPB; ++i) {
-            const int32_t y = (cur[i].x * p.hkv + u.kvh) * p.ps + cur[i].y;   // {page, row_off, pos0, count}
+            y[i] = (cur[i].x * p.hkv + u.kvh) * p.ps + cur[i].y;   // {page, row_off, pos0, count}
 #pragma unroll
-            for (int c = 0; c < CH; ++c) {
-              ptx::tma_load_2d(kst + c * DN_KCHUNK + i * BOX * 128, &tmk, &kv_full[s], c * 64, y);
-              ptx::tma_load_2d(vst + c * DN_KCHUNK + i * BOX * 128, &tmv, &kv_full[s], c * 64, y);
-            }
+            for (int c = 0; c < CH; ++c) ptx::tma_load_2d(kst + c * DN_KCHUNK + i * BOX * 128, &tmk, &k_full[s], c * 64, y[i]);
           }
+          if (kit > 0) issue_v(kit - 1);
+#pragma unroll
+          for (int i = 0; i < EPB; ++i) yprev[i] = y[i];
           if (j + 1 < nb) load_block(u, j + 1);
           else if (ui_next < p.n_units) load_block(un, 0);
         }
         ui = ui_next;
         u = un;
       }
+      if (kit > 0) issue_v(kit - 1);
     }
   } else if (warp == 3) {
     // ===================== Q loader: next unit's rows as soon as its last QK is issued =====
@@ -291,11 +287,11 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       const uint64_t qd0 = ptx::umma_desc_sw128(ptx::smem_u32(smem + L.q0), 16, 1024);
       const uint32_t q_lo0 = (uint32_t)qd0, q_hi = (uint32_t)(qd0 >> 32);
       const uint32_t q_lo1 = (uint32_t)ptx::umma_desc_sw128(ptx::smem_u32(smem + L.q1), 16, 1024);
-      const uint64_t kd0 = ptx::umma_desc_sw128(ptx::smem_u32(smem + L.stage0), 16, 1024);
+      const uint64_t kd0 = ptx::umma_desc_sw128(ptx::smem_u32(smem + L.k0), 16, 1024);
       const uint32_t k_lo0 = (uint32_t)kd0, k_hi = (uint32_t)(kd0 >> 32);
-      const uint64_t vd0 = ptx::umma_desc_sw128(ptx::smem_u32(smem + L.stage0 + CH * DN_KCHUNK), DN_KCHUNK, 1024);
+      const uint64_t vd0 = ptx::umma_desc_sw128(ptx::smem_u32(smem + L.v0), DN_KCHUNK, 1024);
       const uint32_t v_lo0 = (uint32_t)vd0, v_hi = (uint32_t)(vd0 >> 32);
-      const uint32_t stage_lo = L.stage_stride >> 4;
+      const uint32_t stage_lo = L.slot >> 4;
       const uint32_t leader = ptx::elect_one();
       uint32_t kit = 0, gu = 0;
       uint32_t pbits = 0;               // parity of the next p_full[tile][buffer] completion (bit pi)
@@ -303,8 +299,12 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         const Unit u = p.units[ui];
         const int nb = (u.entry_end - u.entry_begin + EPB - 1) / EPB;
         const int ntile = u.n_rows > 128 ? 2 : 1;
-        auto wait_kv = [&](int j) {
-          ptx::mbar_wait(&kv_full[(kit + j) % NS], ((kit + j) / NS) & 1);
+        auto wait_k = [&](int j) {
+          ptx::mbar_wait(&k_full[(kit + j) % NS], ((kit + j) / NS) & 1);
+          ptx::tc_fence_after();
+        };
+        auto wait_v = [&](int j) {
+          ptx::mbar_wait(&v_full[(kit + j) % NS], ((kit + j) / NS) & 1);
           ptx::tc_fence_after();
         };
         auto issue_qk = [&](int t, int j) {
@@ -320,14 +320,60 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         ptx::mbar_wait(q_full, gu & 1);
         ptx::tc_fence_after();
         if (gu == 0 && lane == 0) trace_stamp(p, 2);
+        {
+          // Key-split unit (<= 128 rows): tile t takes the blocks j = t (mod 2) of the one Q
+          // tile (both read Q tile A), local block i = j / 2 in its S buffer i & 1, so the two
+          // tiles ping-pong over one K/V stream; the softmax merges their partial O at the
+          // end.  QK(j+4) is issued after PV(j) (the tile's next-but-one block); its K slot
+          // was freed by QK(j).
+          auto issue_qk_ks = [&](int j) {
+            const int t = j & 1, b = (j >> 1) & 1;
+            const uint32_t klo = k_lo0 + ((kit + j) % NS) * stage_lo;
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk)
+              ptx::umma_ss_lohi(leader, tmem + t * 128 + b * DN_KB, q_lo0 + (((kk / 4) * DN_QCHUNK + (kk % 4) * 32) >> 4),
+                                q_hi, klo + (((kk / 4) * DN_KCHUNK + (kk % 4) * 32) >> 4), k_hi, IDESC_QK, kk > 0);
+            ptx::umma_commit_if(leader, &s_full[t * 2 + b]);
+            ptx::umma_commit_if(leader, &k_empty[(kit + j) % NS]);
+          };
+          for (int j = 0; j < 4 && j < nb; ++j) {
+            wait_k(j);
+            issue_qk_ks(j);
+          }
+          if (nb <= 4) ptx::umma_commit_if(leader, q_empty);
+          for (int j = 0; j < nb; ++j) {
+            const int t = j & 1, b = (j >> 1) & 1, pi = t * 2 + b;
+            wait_v(j);
+            ptx::mbar_wait(&p_full[pi], (pbits >> pi) & 1);
+            pbits ^= 1u << pi;
+            ptx::tc_fence_after();
+            const uint32_t vlo = v_lo0 + ((kit + j) % NS) * stage_lo;
+#pragma unroll
+            for (int kk = 0; kk < DN_KB / 16; ++kk)
+              ptx::umma_ts_lohi(leader, tmem + 256 + t * D, tmem + t * 128 + b * DN_KB + kk * 8,
+                                vlo + ((kk * 16 * 128) >> 4), v_hi, IDESC_PV, (j > 1 || kk > 0) ? 1u : 0u);
+            ptx::umma_commit_if(leader, &o_done[pi]);
+            if (j + 4 < nb) {
+              wait_k(j + 4);
+              issue_qk_ks(j + 4);
+            }
+            if (j + 5 == nb) ptx::umma_commit_if(leader, q_empty);   // QK(nb-1) issued
+            ptx::umma_commit_if(leader, &v_empty[(kit + j) % NS]);
+          }
+          kit += nb;
+          ++gu;
+          continue;
+        }
         for (int j = 0; j < 2 && j < nb; ++j) {
-          wait_kv(j);
+          wait_k(j);
           for (int t = 0; t < ntile; ++t) issue_qk(t, j);
+          ptx::umma_commit_if(leader, &k_empty[(kit + j) % NS]);   // every QK(j) issued
         }
         if (nb <= 2) ptx::umma_commit_if(leader, q_empty);   // every QK of the unit issued: Q may be reloaded
         for (int j = 0; j < nb; ++j) {
           const uint32_t vlo = v_lo0 + ((kit + j) % NS) * stage_lo;
-          if (j + 2 < nb) wait_kv(j + 2);
+          wait_v(j);
+          if (j + 2 < nb) wait_k(j + 2);
           for (int t = 0; t < ntile; ++t) {
             const int pi = t * 2 + (j & 1);
             ptx::mbar_wait(&p_full[pi], (pbits >> pi) & 1);
@@ -342,7 +388,8 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
             if (j + 2 < nb) issue_qk(t, j + 2);
           }
           if (j + 3 == nb) ptx::umma_commit_if(leader, q_empty);   // QK(nb-1) of every tile issued
-          ptx::umma_commit_if(leader, &kv_empty[(kit + j) % NS]);
+          if (j + 2 < nb) ptx::umma_commit_if(leader, &k_empty[(kit + j + 2) % NS]);   // every QK(j+2) issued
+          ptx::umma_commit_if(leader, &v_empty[(kit + j) % NS]);   // every PV(j) issued
         }
         kit += nb;
         ++gu;
@@ -356,7 +403,6 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
     const int r = threadIdx.x - 128 - 128 * t;        // row within the tile = TMEM lane
     const uint32_t lane_base = (uint32_t)(((warp - 4) & 3) * 32) << 16;
     const uint32_t col_o = 256 + t * D;
-    uint32_t sb = 0;                                  // blocks of this tile processed so far
 #if BLEND_TRACE_UNITS
     long long ph_acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};   // per fast block: two-tile [4], single-tile [4], counts [2]
     long long cu_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // clock64 sums: start->S0, S0->last P, epilogue, gap; blocks; units;
@@ -375,11 +421,18 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         enext[i] = v;
       }
     };
+    uint32_t sbase = 0;                               // stream index of the unit's first block (K / V slots)
     for (int uk = 0, ui = snake_unit(0); ui < p.n_units; ui = snake_unit(++uk)) {
       const Unit u = p.units[ui];
       const int nb = (u.entry_end - u.entry_begin + EPB - 1) / EPB;
-      if (t == 1 && u.n_rows <= 128) continue;       // tile B idle for this unit
-      const int row = 128 * t + r;                    // row within the unit
+      // key-split unit (<= 128 rows, >= 2 blocks): both tiles serve the same rows, tile t
+      // the blocks j = t (mod 2); the partial results are merged at the epilogue
+      constexpr bool ks = true;   // every unit of this launch is a key-split unit (planner)
+      if (t == 1 && u.n_rows <= 128 && !ks) {         // tile B idle for this unit
+        sbase += nb;
+        continue;
+      }
+      const int row = (ks ? 0 : 128 * t) + r;         // row within the unit
 #if BLEND_TRACE_UNITS
       if (threadIdx.x == 128 && uk < 10) trace_stamp(p, 20 + 4 * uk);
       const long long cu0 = clock64();
@@ -402,17 +455,18 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       // softmax: its P rows only feed its own (never stored) O rows, so they may hold
       // anything; it keeps the barrier protocol
       const bool warp_pad = __all_sync(0xffffffffu, !row_ok);
-      load_meta(u, 0);
-      for (int j = 0; j < nb; ++j, ++sb) {
-        const int buf = j & 1;
+      const int jstep = ks ? 2 : 1;
+      int nloc = 0;                                   // blocks this tile processes in this unit
+      load_meta(u, ks ? t : 0);
+      for (int j = ks ? t : 0; j < nb; j += jstep, ++nloc) {
+        const int buf = nloc & 1;
         const uint32_t col_s = t * 128 + buf * DN_KB;
-        // key positions of this block from the stage metadata the producer wrote (the
-        // stage cannot be refilled before this block's P is consumed)
+        const uint32_t sb = sbase + j;                // stream index of block j (its K / V slot)
         // this block's {pos0, count} were loaded one block ahead (latency off the critical path)
         int2 ecur[EPB];
 #pragma unroll
         for (int i = 0; i < EPB; ++i) ecur[i] = enext[i];
-        if (j + 1 < nb) load_meta(u, j + 1);
+        if (j + jstep < nb) load_meta(u, j + jstep);
         int vis[EPB];
         bool full_vis = true;
 #pragma unroll
@@ -438,13 +492,15 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         // Entries with count < BOX (a node's last page, padding entries): their V rows past
         // the count may hold anything, NaN included, and the PV MMA would multiply them by
         // P = 0 -> tile A's warpgroup zeroes them before its P hand-off (the PV MMAs of both
-        // tiles are issued after it).  K rows past the count only reach masked scores.
-        if (t == 0) {
+        // tiles are issued after it; in a key-split unit each tile zeroes its own blocks).
+        // K rows past the count only reach masked scores.
+        if (t == 0 || ks) {
           bool part = false;
 #pragma unroll
           for (int i = 0; i < EPB; ++i) part = part || ecur[i].y < BOX;
           if (part) {
-            uint8_t* vst = smem + L.stage0 + (sb % NS) * L.stage_stride + CH * DN_KCHUNK;
+            ptx::mbar_wait(&v_full[sb % NS], (sb / NS) & 1);   // V(j) has landed (K and V arrive separately)
+            uint8_t* vst = smem + L.v0 + (sb % NS) * L.slot;
 #pragma unroll
             for (int i = 0; i < EPB; ++i) {
               const int nz = BOX - ecur[i].y;
@@ -523,7 +579,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         if (p.stats != nullptr && lane == 0) {   // diagnostics: blocks per softmax path
           stat_add(p, STAT_DENSE_BLOCKS, 1);
           if (slow) stat_add(p, STAT_DENSE_SLOW, 1);
-          if (slow && j > 0) stat_add(p, STAT_DENSE_SLOW_LATE, 1);
+          if (slow && nloc > 0) stat_add(p, STAT_DENSE_SLOW_LATE, 1);
         }
         if (slow) {
         float mxv[8];
@@ -535,12 +591,12 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
                                fmaxf(fmaxf(mxv[4], mxv[5]), fmaxf(mxv[6], mxv[7])));
         const float mx2 = mx * p.scale_log2;
         const bool need = mx2 > m_ref + DN_RESCALE_T;
-        if (j > 0 && __any_sync(0xffffffffu, need)) {
+        if (nloc > 0 && __any_sync(0xffffffffu, need)) {
           if (lane == 0) stat_add(p, STAT_DENSE_RESCALE, 1);
           // O holds PV up to block j-1: wait for it.  Parity is unambiguous because the
           // previous completion on this barrier (PV(j-3)) is certified by s_full(j-1) and
           // PV(j+1) cannot be issued before this block's P.
-          const int pb_ = (j - 1) & 1;
+          const int pb_ = (nloc - 1) & 1;
           ptx::mbar_wait(&o_done[t * 2 + pb_], ((pb_ ? scnt1 : scnt0) - 1) & 1);
           ptx::tc_fence_after();
           const float alpha = need ? ptx::ex2(m_ref - mx2) : 1.f;
@@ -601,14 +657,47 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       // ---- epilogue: PV of the unit's last block done (MMAs complete in issue order, so
       // this also certifies every earlier PV of the unit)
       {
-        const int lb = (nb - 1) & 1;
+        const int lb = (nloc - 1) & 1;
         ptx::mbar_wait(&o_done[t * 2 + lb], ((lb ? scnt1 : scnt0) - 1) & 1);
       }
       ptx::tc_fence_after();
       if (threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 60);
-      const float m_use = m_ref == -INFINITY ? 0.f : m_ref;
-      const float inv = l > 0.f ? 1.f / l : 0.f;
-      const float lse2 = l > 0.f ? m_use + log2f(l) : -INFINITY;
+      // Key-split unit: tile B hands its row state (m, l) to tile A through its staging
+      // tile (named barrier per lane quarter, 64 threads) and waits until tile A has read
+      // O_B out of TMEM; tile A merges the two partials: O = (2^(mA-m) O_A + 2^(mB-m) O_B)
+      // / (2^(mA-m) lA + 2^(mB-m) lB), lse = m + log2(...).
+      const int q4 = (warp - 4) & 3;
+      if (ks && t == 1) {
+        float* xs = reinterpret_cast<float*>(smem + L.stg + (warp - 4) * 4096);
+        xs[lane] = m_ref;
+        xs[32 + lane] = l;
+        ptx::tc_fence_before();
+        ptx::bar_sync(1 + q4, 64);   // (m, l) and O_B are ready
+        ptx::bar_sync(5 + q4, 64);   // tile A has read O_B (the next unit's PV may overwrite it)
+        sbase += nb;
+        continue;
+      }
+      float sA, sB = 0.f, lse2;       // O = sA O_A + sB O_B
+      if (ks) {
+        ptx::bar_sync(1 + q4, 64);
+        ptx::tc_fence_after();
+        const float* xs = reinterpret_cast<const float*>(smem + L.stg + warp * 4096);   // tile B warp q4's tile
+        const float mB = xs[lane], lB = xs[32 + lane];
+        const float mx = fmaxf(m_ref, mB);
+        const float mu = mx == -INFINITY ? 0.f : mx;
+        const float aA = m_ref == -INFINITY ? 0.f : ptx::ex2(m_ref - mu);
+        const float aB = mB == -INFINITY ? 0.f : ptx::ex2(mB - mu);
+        const float lt = l * aA + lB * aB;
+        const float iv = lt > 0.f ? 1.f / lt : 0.f;
+        sA = aA * iv;
+        sB = aB * iv;
+        lse2 = lt > 0.f ? mu + log2f(lt) : -INFINITY;
+      } else {
+        const float m_use = m_ref == -INFINITY ? 0.f : m_ref;
+        sA = l > 0.f ? 1.f / l : 0.f;
+        lse2 = l > 0.f ? m_use + log2f(l) : -INFINITY;
+      }
+      const float inv = ks ? 1.f : sA;
       // O / l leaves through a per-warp smem staging tile (XOR-swizzled 16-B units, no
       // bank conflicts), so that every global store instruction writes whole row
       // segments of 4 rows instead of 32 scattered pieces.  Row kinds: 2 = fp32 partial
@@ -638,6 +727,15 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
          uint32_t ov2[64];
          ptx::tmem_ld32(tmem + lane_base + col_o + hh * 64, ov2);
          ptx::tmem_ld32(tmem + lane_base + col_o + hh * 64 + 32, ov2 + 32);
+         if (ks) {   // sA O_A + sB O_B (inv = 1 below)
+           uint32_t ob2[64];
+           ptx::tmem_ld32(tmem + lane_base + 256 + D + hh * 64, ob2);
+           ptx::tmem_ld32(tmem + lane_base + 256 + D + hh * 64 + 32, ob2 + 32);
+           ptx::tmem_wait_ld();
+#pragma unroll
+           for (int k = 0; k < 64; ++k)
+             ov2[k] = __float_as_uint(fmaf(__uint_as_float(ob2[k]), sB, __uint_as_float(ov2[k]) * sA));
+         }
          ptx::tmem_wait_ld();
          if (hh == 0 && threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 62);
          if (all_bf16) {
@@ -685,6 +783,10 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
          }
         }
       }
+      if (ks) {                       // O_B has been read: tile B may go on (its next PV overwrites O_B)
+        ptx::tc_fence_before();
+        ptx::bar_sync(5 + q4, 64);
+      }
       if (threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 61);
       if (tgt == PM_DIRECT) p.lse[(int64_t)token * p.hq + head] = lse2 * kLn2;
       else if (tgt >= 0) p.ws_lse[(int64_t)tgt * p.hq + head] = lse2;
@@ -695,6 +797,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       cu_prev_end = clock64();
       cu_acc[2] += cu_prev_end - cu_lp;
 #endif
+      sbase += nb;
     }
 #if BLEND_TRACE_UNITS
     if (threadIdx.x == 128 && p.trace != nullptr) {
@@ -711,7 +814,13 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, DN_TMEM_COLS);
   }
+  // this grid (a PDL dependent of the streaming grid, itself a dependent of the two-tile
+  // dense grid) completes only after both, so the merge grid that depends on it sees every
+  // partial row
+  ptx::pdl_wait();
 }
+
+}  // namespace ks
 
 cudaError_t make_cache_tmap(CUtensorMap* m, const void* base, int64_t rows, int D, int box_rows);
 cudaError_t make_q_tmap(CUtensorMap* m, const void* base, int64_t T, int hq, int D, int g, int box_tok);
@@ -719,7 +828,7 @@ cudaError_t set_smem_once(const void* func, size_t bytes);
 int num_sms_cached();
 
 template <int D, int BOX>
-static cudaError_t launch_dense_db(const AttnParams& p, int64_t n_cache_pages, cudaStream_t st) {
+static cudaError_t launch_dense_ks_db(const AttnParams& p, int64_t n_cache_pages, cudaStream_t st, bool overlap) {
   CUtensorMap tk, tv;
   const int64_t rows = n_cache_pages * p.hkv * p.ps;
   cudaError_t e = make_cache_tmap(&tk, p.k_cache, rows, D, BOX);
@@ -734,28 +843,35 @@ static cudaError_t launch_dense_db(const AttnParams& p, int64_t n_cache_pages, c
     if (e == cudaSuccess) e = make_q_tmap(&tq1, p.q, p.n_tokens, p.hq, D, p.g, 1);
     if (e != cudaSuccess) return e;
   }
-  const size_t smem = dense_layout(D).total + 1024;
-  e = set_smem_once((const void*)dense_kernel<D, BOX>, smem);
+  const size_t smem = ks::dense_layout(D).total + 1024;
+  e = set_smem_once((const void*)ks::dense_ks_kernel<D, BOX>, smem);
   if (e != cudaSuccess) return e;
-  int grid = p.n_units < num_sms_cached() ? p.n_units : num_sms_cached();
-  if (p.dense_ctas > 0 && grid > p.dense_ctas) grid = p.dense_ctas;   // planner: SMs left to streaming
-  dense_kernel<D, BOX><<<grid, DN_THREADS, smem, st>>>(tk, tv, tq, tq1, p);
-  return cudaPeekAtLastError();
+  const int grid = p.n_units < num_sms_cached() ? p.n_units : num_sms_cached();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(ks::DN_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = overlap ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, ks::dense_ks_kernel<D, BOX>, tk, tv, tq, tq1, p);
 }
 
 template <int D>
-static cudaError_t launch_dense_d(const AttnParams& p, int64_t n_cache_pages, cudaStream_t st) {
-  if (p.ps >= 64) return launch_dense_db<D, 64>(p, n_cache_pages, st);
-  if (p.ps == 32) return launch_dense_db<D, 32>(p, n_cache_pages, st);
-  return launch_dense_db<D, 16>(p, n_cache_pages, st);
+static cudaError_t launch_dense_ks_d(const AttnParams& p, int64_t n_cache_pages, cudaStream_t st, bool overlap) {
+  if (p.ps >= 64) return launch_dense_ks_db<D, 64>(p, n_cache_pages, st, overlap);
+  if (p.ps == 32) return launch_dense_ks_db<D, 32>(p, n_cache_pages, st, overlap);
+  return launch_dense_ks_db<D, 16>(p, n_cache_pages, st, overlap);
 }
 
-cudaError_t launch_generic(const AttnParams& p, cudaStream_t st);
-
-cudaError_t launch_dense(const AttnParams& p, int64_t n_cache_pages, cudaStream_t st) {
+// Key-split units (planner section SEC_DENSE_KS); p.units / p.dqtok / p.n_units describe them.
+cudaError_t launch_dense_ks(const AttnParams& p, int64_t n_cache_pages, cudaStream_t st, bool overlap) {
   if (p.n_units <= 0) return cudaSuccess;
-  if (p.kv_f32) return launch_generic(p, st);
-  return p.d == 128 ? launch_dense_d<128>(p, n_cache_pages, st) : launch_dense_d<64>(p, n_cache_pages, st);
+  return p.d == 128 ? launch_dense_ks_d<128>(p, n_cache_pages, st, overlap)
+                    : launch_dense_ks_d<64>(p, n_cache_pages, st, overlap);
 }
 
 }  // namespace blend

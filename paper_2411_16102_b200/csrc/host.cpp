@@ -835,6 +835,30 @@ int build_plan(blend_tree* t) {
       if (consec) dqtok[ui] = t0;
     }
 
+  // Key-split units: <= 128 rows (one Q tile) and >= 2 64-key blocks run in dense_ks.cu,
+  // where the CTA's two tiles take alternate blocks of the one tile and merge at the end
+  // (a separate launch; both lists keep the longest-first order).
+  std::vector<blend::Unit> dunits_ks;
+  std::vector<int32_t> dqtok_ks;
+  {
+    const int32_t epb = 64 / std::min<int32_t>(a.page_size, 64);
+    std::vector<blend::Unit> keep;
+    std::vector<int32_t> keep_q;
+    for (size_t ui = 0; ui < dunits.size(); ++ui) {
+      const blend::Unit& u = dunits[ui];
+      const int32_t nb = (u.entry_end - u.entry_begin + epb - 1) / epb;
+      if (u.n_rows <= 128 && nb >= 2 && a.kv_dtype == BLEND_BF16) {
+        dunits_ks.push_back(u);
+        dqtok_ks.push_back(dqtok[ui]);
+      } else {
+        keep.push_back(u);
+        keep_q.push_back(dqtok[ui]);
+      }
+    }
+    dunits.swap(keep);
+    dqtok.swap(keep_q);
+  }
+
   // Per-row descriptors of the streaming units (STREAM_ROWS slots per unit): the
   // kernel gets each row's q/out row, position and partmap target in one load
   // instead of the item_tokens -> tok_pos / partmap chain.
@@ -875,6 +899,8 @@ int build_plan(blend_tree* t) {
   put(SEC_MERGE_OFF, merge_off.data(), 4, merge_off.size());
   put(SEC_STREAM_ROWS, srows.data(), sizeof(RowDesc), srows.size());
   put(SEC_DENSE_QTOK, dqtok.data(), 4, dqtok.size());
+  put(SEC_DENSE_KS, dunits_ks.data(), sizeof(Unit), dunits_ks.size());
+  put(SEC_DENSE_KS_QTOK, dqtok_ks.data(), 4, dqtok_ks.size());
   blob.resize((blob.size() + 255) & ~size_t(255));
 
   t->n_partial_rows = prow;
@@ -884,7 +910,7 @@ int build_plan(blend_tree* t) {
   t->workspace_bytes = o_bytes + (((size_t)prow * hq * 4 + 255) & ~size_t(255)) + 256;
   t->info.n_tokens = T;
   t->info.n_items = (int64_t)items.size();
-  t->info.n_dense_units = (int64_t)dunits.size();
+  t->info.n_dense_units = (int64_t)(dunits.size() + dunits_ks.size());
   t->info.n_stream_units = (int64_t)sunits.size();
   t->info.n_partial_rows = prow;
   t->info.n_merge_tokens = (int64_t)merge_tok.size();

@@ -20,6 +20,9 @@ enum PlanSection {
   SEC_STREAM_ROWS,     // RowDesc[n_stream * STREAM_ROWS]  per-row descriptors of the streaming units
   SEC_DENSE_QTOK,      // int32[n_dense]  first token of a dense unit whose tokens are consecutive
                        //                 (its Q tiles load by TMA boxes), else -1
+  SEC_DENSE_KS,        // Unit[n_ks]      dense units of <= 128 rows and >= 2 blocks, run key-split
+                       //                 by dense_ks.cu (same layout as SEC_DENSE_UNITS)
+  SEC_DENSE_KS_QTOK,   // int32[n_ks]     SEC_DENSE_QTOK of those units
   SEC_COUNT
 };
 

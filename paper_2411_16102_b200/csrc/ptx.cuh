@@ -43,6 +43,10 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 }
 // Wait for the phase with the given parity.  Watchdog: a wait that exceeds 10 s is a
 // protocol bug (a hang) — trap so the launch fails with an error instead of hanging.
+// named barrier `id` (1..15) over `count` threads (a multiple of 32)
+__device__ __forceinline__ void bar_sync(uint32_t id, uint32_t count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
   const uint64_t t0 = globaltimer_ns();

@@ -16,7 +16,7 @@ from oracle import attention as A
 from synth import values as V
 
 SEC = ["tok_pos", "item_tok_off", "item_tokens", "entries", "dunits", "sunits", "partmap",
-       "merge_tok", "merge_off", "stream_rows", "dense_qtok"]
+       "merge_tok", "merge_off", "stream_rows", "dense_qtok", "dunits_ks", "dense_ks_qtok"]
 
 
 def plan_image(tree):
@@ -31,7 +31,7 @@ def plan_image(tree):
     blob = np.ctypeslib.as_array(C.cast(data, C.POINTER(C.c_uint8)), (nbytes.value,)).copy() \
         if nbytes.value else np.zeros(0, np.uint8)
     secs = {}
-    width = {"entries": 4, "dunits": 8, "sunits": 8, "stream_rows": 4}
+    width = {"entries": 4, "dunits": 8, "sunits": 8, "stream_rows": 4, "dunits_ks": 8}
     for i, name in enumerate(SEC):
         o, n = int(off[i]), int(cnt[i])
         k = width.get(name, 1)
@@ -61,13 +61,24 @@ def check_stream_rows(P, g, Hq):
                                               int(P["partmap"][pmb + tl]), kvh * g + j)
 
 
-def check_dense_qtok(P, g):
+def check_dense_qtok(P, g, ps):
     """A dense unit marked for TMA Q loading (first token t0 >= 0) covers whole tokens
     t0, t0+1, ... of q; every unit with consecutive whole tokens is marked when its
-    128-row tiles hold whole tokens."""
-    qt = P["dense_qtok"]
-    assert len(qt) == len(P["dunits"])
-    for ui, u in enumerate(P["dunits"]):
+    128-row tiles hold whole tokens.  Key-split units (dense_ks.cu) are exactly the bf16
+    units of <= 128 rows and >= 2 64-key blocks."""
+    epb = 64 // min(ps, 64)
+    for name, qname, ks in (("dunits", "dense_qtok", False), ("dunits_ks", "dense_ks_qtok", True)):
+        for u in P[name]:
+            nr, ne = int(u[3]), int(u[5]) - int(u[4])
+            assert (nr <= 128 and (ne + epb - 1) // epb >= 2) == ks or (not ks and len(P["dunits_ks"]) == 0), \
+                (name, nr, ne)
+    _check_qtok(P["dense_qtok"], P["dunits"], P, g)
+    _check_qtok(P["dense_ks_qtok"], P["dunits_ks"], P, g)
+
+
+def _check_qtok(qt, dunits, P, g):
+    assert len(qt) == len(dunits)
+    for ui, u in enumerate(dunits):
         item, kvh, rb, nr, eb, ee, pmb, tb = (int(x) for x in u)
         toks = [int(P["item_tokens"][tb + tl]) for tl in range(rb // g, (rb + nr - 1) // g + 1)]
         consec = rb % g == 0 and toks == list(range(toks[0], toks[0] + len(toks)))
@@ -96,8 +107,8 @@ def simulate(w, tree):
     lse = np.full((T, Hq), np.nan)
     written = np.zeros((T, Hq), dtype=np.int64)
     check_stream_rows(P, g, Hq)
-    check_dense_qtok(P, g)
-    for kind, units in (("dense", P["dunits"]), ("stream", P["sunits"])):
+    check_dense_qtok(P, g, ps)
+    for kind, units in (("dense", P["dunits"]), ("dense", P["dunits_ks"]), ("stream", P["sunits"])):
         for u in units:
             item, kvh, rb, nr, eb, ee, pmb, tb = (int(x) for x in u)
             kpos, K, Vv = [], [], []
