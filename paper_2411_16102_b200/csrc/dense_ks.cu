@@ -286,7 +286,6 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       // lo = start address >> 4 | LBO >> 4 << 16, advanced by immediates
       const uint64_t qd0 = ptx::umma_desc_sw128(ptx::smem_u32(smem + L.q0), 16, 1024);
       const uint32_t q_lo0 = (uint32_t)qd0, q_hi = (uint32_t)(qd0 >> 32);
-      const uint32_t q_lo1 = (uint32_t)ptx::umma_desc_sw128(ptx::smem_u32(smem + L.q1), 16, 1024);
       const uint64_t kd0 = ptx::umma_desc_sw128(ptx::smem_u32(smem + L.k0), 16, 1024);
       const uint32_t k_lo0 = (uint32_t)kd0, k_hi = (uint32_t)(kd0 >> 32);
       const uint64_t vd0 = ptx::umma_desc_sw128(ptx::smem_u32(smem + L.v0), DN_KCHUNK, 1024);
@@ -298,7 +297,6 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       for (int uk = 0, ui = snake_unit(0); ui < p.n_units; ui = snake_unit(++uk)) {
         const Unit u = p.units[ui];
         const int nb = (u.entry_end - u.entry_begin + EPB - 1) / EPB;
-        const int ntile = u.n_rows > 128 ? 2 : 1;
         auto wait_k = [&](int j) {
           ptx::mbar_wait(&k_full[(kit + j) % NS], ((kit + j) / NS) & 1);
           ptx::tc_fence_after();
@@ -307,21 +305,11 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
           ptx::mbar_wait(&v_full[(kit + j) % NS], ((kit + j) / NS) & 1);
           ptx::tc_fence_after();
         };
-        auto issue_qk = [&](int t, int j) {
-          const uint32_t qlo = t ? q_lo1 : q_lo0;
-          const uint32_t klo = k_lo0 + ((kit + j) % NS) * stage_lo;
-          const uint32_t dcol = tmem + t * 128 + (j & 1) * DN_KB;
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk)
-            ptx::umma_ss_lohi(leader, dcol, qlo + (((kk / 4) * DN_QCHUNK + (kk % 4) * 32) >> 4), q_hi,
-                              klo + (((kk / 4) * DN_KCHUNK + (kk % 4) * 32) >> 4), k_hi, IDESC_QK, kk > 0);
-          ptx::umma_commit_if(leader, &s_full[t * 2 + (j & 1)]);
-        };
         ptx::mbar_wait(q_full, gu & 1);
         ptx::tc_fence_after();
         if (gu == 0 && lane == 0) trace_stamp(p, 2);
         {
-          // Key-split unit (<= 128 rows): tile t takes the blocks j = t (mod 2) of the one Q
+          // tile t takes the blocks j = t (mod 2) of the one Q
           // tile (both read Q tile A), local block i = j / 2 in its S buffer i & 1, so the two
           // tiles ping-pong over one K/V stream; the softmax merges their partial O at the
           // end.  QK(j+4) is issued after PV(j) (the tile's next-but-one block); its K slot
@@ -360,36 +348,6 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
             if (j + 5 == nb) ptx::umma_commit_if(leader, q_empty);   // QK(nb-1) issued
             ptx::umma_commit_if(leader, &v_empty[(kit + j) % NS]);
           }
-          kit += nb;
-          ++gu;
-          continue;
-        }
-        for (int j = 0; j < 2 && j < nb; ++j) {
-          wait_k(j);
-          for (int t = 0; t < ntile; ++t) issue_qk(t, j);
-          ptx::umma_commit_if(leader, &k_empty[(kit + j) % NS]);   // every QK(j) issued
-        }
-        if (nb <= 2) ptx::umma_commit_if(leader, q_empty);   // every QK of the unit issued: Q may be reloaded
-        for (int j = 0; j < nb; ++j) {
-          const uint32_t vlo = v_lo0 + ((kit + j) % NS) * stage_lo;
-          wait_v(j);
-          if (j + 2 < nb) wait_k(j + 2);
-          for (int t = 0; t < ntile; ++t) {
-            const int pi = t * 2 + (j & 1);
-            ptx::mbar_wait(&p_full[pi], (pbits >> pi) & 1);
-            pbits ^= 1u << pi;
-            ptx::tc_fence_after();
-            const uint32_t acol = tmem + t * 128 + (j & 1) * DN_KB;
-#pragma unroll
-            for (int kk = 0; kk < DN_KB / 16; ++kk)
-              ptx::umma_ts_lohi(leader, tmem + 256 + t * D, acol + kk * 8, vlo + ((kk * 16 * 128) >> 4), v_hi,
-                                IDESC_PV, (j > 0 || kk > 0) ? 1u : 0u);
-            ptx::umma_commit_if(leader, &o_done[pi]);
-            if (j + 2 < nb) issue_qk(t, j + 2);
-          }
-          if (j + 3 == nb) ptx::umma_commit_if(leader, q_empty);   // QK(nb-1) of every tile issued
-          if (j + 2 < nb) ptx::umma_commit_if(leader, &k_empty[(kit + j + 2) % NS]);   // every QK(j+2) issued
-          ptx::umma_commit_if(leader, &v_empty[(kit + j) % NS]);   // every PV(j) issued
         }
         kit += nb;
         ++gu;
@@ -425,14 +383,9 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
     for (int uk = 0, ui = snake_unit(0); ui < p.n_units; ui = snake_unit(++uk)) {
       const Unit u = p.units[ui];
       const int nb = (u.entry_end - u.entry_begin + EPB - 1) / EPB;
-      // key-split unit (<= 128 rows, >= 2 blocks): both tiles serve the same rows, tile t
-      // the blocks j = t (mod 2); the partial results are merged at the epilogue
-      constexpr bool ks = true;   // every unit of this launch is a key-split unit (planner)
-      if (t == 1 && u.n_rows <= 128 && !ks) {         // tile B idle for this unit
-        sbase += nb;
-        continue;
-      }
-      const int row = (ks ? 0 : 128 * t) + r;         // row within the unit
+      // both tiles serve the unit's rows, tile t the blocks j = t (mod 2); the partial
+      // results are merged at the epilogue
+      const int row = r;                              // row within the unit
 #if BLEND_TRACE_UNITS
       if (threadIdx.x == 128 && uk < 10) trace_stamp(p, 20 + 4 * uk);
       const long long cu0 = clock64();
@@ -455,10 +408,9 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       // softmax: its P rows only feed its own (never stored) O rows, so they may hold
       // anything; it keeps the barrier protocol
       const bool warp_pad = __all_sync(0xffffffffu, !row_ok);
-      const int jstep = ks ? 2 : 1;
       int nloc = 0;                                   // blocks this tile processes in this unit
-      load_meta(u, ks ? t : 0);
-      for (int j = ks ? t : 0; j < nb; j += jstep, ++nloc) {
+      load_meta(u, t);
+      for (int j = t; j < nb; j += 2, ++nloc) {
         const int buf = nloc & 1;
         const uint32_t col_s = t * 128 + buf * DN_KB;
         const uint32_t sb = sbase + j;                // stream index of block j (its K / V slot)
@@ -466,7 +418,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         int2 ecur[EPB];
 #pragma unroll
         for (int i = 0; i < EPB; ++i) ecur[i] = enext[i];
-        if (j + jstep < nb) load_meta(u, j + jstep);
+        if (j + 2 < nb) load_meta(u, j + 2);
         int vis[EPB];
         bool full_vis = true;
 #pragma unroll
@@ -494,7 +446,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         // P = 0 -> tile A's warpgroup zeroes them before its P hand-off (the PV MMAs of both
         // tiles are issued after it; in a key-split unit each tile zeroes its own blocks).
         // K rows past the count only reach masked scores.
-        if (t == 0 || ks) {
+        {
           bool part = false;
 #pragma unroll
           for (int i = 0; i < EPB; ++i) part = part || ecur[i].y < BOX;
@@ -667,7 +619,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       // O_B out of TMEM; tile A merges the two partials: O = (2^(mA-m) O_A + 2^(mB-m) O_B)
       // / (2^(mA-m) lA + 2^(mB-m) lB), lse = m + log2(...).
       const int q4 = (warp - 4) & 3;
-      if (ks && t == 1) {
+      if (t == 1) {
         float* xs = reinterpret_cast<float*>(smem + L.stg + (warp - 4) * 4096);
         xs[lane] = m_ref;
         xs[32 + lane] = l;
@@ -678,7 +630,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         continue;
       }
       float sA, sB = 0.f, lse2;       // O = sA O_A + sB O_B
-      if (ks) {
+      {
         ptx::bar_sync(1 + q4, 64);
         ptx::tc_fence_after();
         const float* xs = reinterpret_cast<const float*>(smem + L.stg + warp * 4096);   // tile B warp q4's tile
@@ -692,12 +644,8 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         sA = aA * iv;
         sB = aB * iv;
         lse2 = lt > 0.f ? mu + log2f(lt) : -INFINITY;
-      } else {
-        const float m_use = m_ref == -INFINITY ? 0.f : m_ref;
-        sA = l > 0.f ? 1.f / l : 0.f;
-        lse2 = l > 0.f ? m_use + log2f(l) : -INFINITY;
       }
-      const float inv = ks ? 1.f : sA;
+      const float inv = 1.f;
       // O / l leaves through a per-warp smem staging tile (XOR-swizzled 16-B units, no
       // bank conflicts), so that every global store instruction writes whole row
       // segments of 4 rows instead of 32 scattered pieces.  Row kinds: 2 = fp32 partial
@@ -727,7 +675,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
          uint32_t ov2[64];
          ptx::tmem_ld32(tmem + lane_base + col_o + hh * 64, ov2);
          ptx::tmem_ld32(tmem + lane_base + col_o + hh * 64 + 32, ov2 + 32);
-         if (ks) {   // sA O_A + sB O_B (inv = 1 below)
+         {           // sA O_A + sB O_B (inv = 1 below)
            uint32_t ob2[64];
            ptx::tmem_ld32(tmem + lane_base + 256 + D + hh * 64, ob2);
            ptx::tmem_ld32(tmem + lane_base + 256 + D + hh * 64 + 32, ob2 + 32);
@@ -783,7 +731,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
          }
         }
       }
-      if (ks) {                       // O_B has been read: tile B may go on (its next PV overwrites O_B)
+      {                               // O_B has been read: tile B may go on (its next PV overwrites O_B)
         ptx::tc_fence_before();
         ptx::bar_sync(5 + q4, 64);
       }
