@@ -26,8 +26,11 @@
 namespace blend {
 namespace ks {
 
+#ifndef DN_KS_NSTAGE128
+#define DN_KS_NSTAGE128 5  // K / V ring slots at D = 128 (64 keys each)
+#endif
 #ifndef DN_NSTAGE128
-#define DN_NSTAGE128 4     // K/V ring stages at D = 128 (64 keys each)
+#define DN_NSTAGE128 4
 #endif
 #ifndef BLEND_TRACE_WARPS
 #define BLEND_TRACE_WARPS 0    // 1: per-warp P hand-off stamps for blocks 20..23 of the first unit
@@ -55,10 +58,10 @@ __host__ __device__ inline DenseSmem dense_layout(int D) {
   DenseSmem L;
   const int CH = D / 64;
   L.q0 = 0;
-  L.q1 = CH * DN_QCHUNK;
+  L.q1 = 0;                              // one Q tile only (both tiles read it)
   L.slot = CH * DN_KCHUNK;               // one 64-key K (or V) block
-  L.nstage = D == 128 ? DN_NSTAGE128 : 8;
-  L.k0 = 2 * CH * DN_QCHUNK;             // K ring, then V ring (a K slot frees at QK, a V slot at PV)
+  L.nstage = D == 128 ? DN_KS_NSTAGE128 : 8;   // the second Q tile's space holds an extra K and V slot
+  L.k0 = CH * DN_QCHUNK;                 // K ring, then V ring (a K slot frees at QK, a V slot at PV)
   L.v0 = L.k0 + L.nstage * L.slot;
   L.bar = L.v0 + L.nstage * L.slot;
   L.stg = L.bar + 512;                    // epilogue staging: per softmax warp 32 rows x 128 B
