@@ -75,7 +75,7 @@ def main(src, dst_prefix):
         wl = os.path.basename(f)[len("launches_"):-4]
         agg = launches(f)
         attn = {k: v for k, v in agg.items() if k.split("::")[-1].split("<")[0] in
-                ("dense_kernel", "stream_kernel", "streamw_kernel", "merge_kernel", "generic_unit_kernel")}
+                ("dense_kernel", "dense_ks_kernel", "stream_kernel", "streamw_kernel", "merge_kernel", "generic_unit_kernel")}
         tot = sum(sum(v) / len(v) for v in attn.values()) or 1.0
         md += [f"## launch list `{wl}` (cold-cache, serialised; per-launch mean)", "",
                "| kernel | launches | mean us | share of attention step |", "|---|---|---|---|"]
