@@ -59,7 +59,7 @@ def load_peaks():
     return d
 
 
-PROFILE_TAG = "r2g"   # profiles/<tag>_ncu.json: ncu --set full captures of this code's kernels
+PROFILE_TAG = "r2j"   # profiles/<tag>_ncu.json: ncu --set full captures of this code's kernels
 
 
 def ncu_traffic(workload: str, kernel: str):
@@ -246,7 +246,10 @@ def _roofline(kind, pw, t_ms, peaks, burst, workload, path_auto):
         tf = pw["dense_flops"] / (t_ms * 1e-3) / 1e12 if t_ms > 0 else 0.0
         peak = peaks["bf16_tflops"] if burst else peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
         traffic, tsrc = ncu_traffic(workload, "dense_kernel") if path_auto else (None, None)
-        return {"kernel": "dense_kernel (tcgen05)" if path_auto else "dense (generic executor)",
+        tks, _ = ncu_traffic(workload, "dense_ks_kernel") if path_auto else (None, None)
+        if traffic is not None and tks is not None:   # the pass = the two-tile and the key-split launch
+            traffic, tsrc = traffic + tks, tsrc + " + [" + workload + "_dense_ks_kernel]"
+        return {"kernel": "dense_kernel + dense_ks_kernel (tcgen05)" if path_auto else "dense (generic executor)",
                 "bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak,
                 "traffic": traffic, "traffic_source": tsrc, "launch_ms": t_ms,
                 "algorithmic_per_launch": pw["dense_flops"], "algorithmic_bytes_per_launch": pw["dense_bytes"],
@@ -467,8 +470,9 @@ def run_ours(args):
         dist.barrier()
 
     # our kernels per timed step: dense + streaming + merge (+ the L2 flush between steps)
-    launches_per_step = int(info["n_dense_units"] > 0) + int(info["n_stream_units"] > 0) + \
-        int(info["n_merge_tokens"] > 0) + int(do_flush)
+    cnt = db.plan.count   # one launch per non-empty pass: two-tile dense, key-split dense, streaming, merge
+    launches_per_step = sum(int(cnt[s_] > 0) for s_ in (B.SEC_DENSE_UNITS, B.SEC_DENSE_KS, B.SEC_STREAM_UNITS,
+                                                        B.SEC_MERGE_TOK)) + int(do_flush)
 
     # ---- rooflines of both passes (per launch, CUDA events on the launching stream)
     peaks = load_peaks()

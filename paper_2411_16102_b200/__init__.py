@@ -63,6 +63,10 @@ class PlanInfo(C.Structure):
         "n_merge_tokens", "n_entries", "dense_kv_tokens", "stream_kv_tokens")]
 
 
+# plan sections (csrc/internal.h order) the bench counts launches from
+SEC_DENSE_UNITS, SEC_STREAM_UNITS, SEC_MERGE_TOK, SEC_DENSE_KS = 4, 5, 7, 11
+
+
 class Plan(C.Structure):
     _fields_ = [("dev", C.c_void_p), ("bytes", C.c_size_t), ("off", C.c_int64 * 16),
                 ("count", C.c_int64 * 16), ("num_q_heads", C.c_int32), ("num_kv_heads", C.c_int32),

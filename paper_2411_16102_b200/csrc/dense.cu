@@ -44,6 +44,10 @@ namespace blend {
 #ifndef DN_NSTAGE128
 #define DN_NSTAGE128 4     // K/V ring stages at D = 128 (64 keys each)
 #endif
+#ifndef DN_REG_CTL
+#define DN_REG_CTL 56      // setmaxnreg of warpgroup 0 (producer, MMA, allocator, Q loader)
+#define DN_REG_SM 224      // setmaxnreg of the softmax warpgroups (56*128 + 224*256 = 64512)
+#endif
 #ifndef BLEND_TRACE_WARPS
 #define BLEND_TRACE_WARPS 0    // 1: per-warp P hand-off stamps for blocks 20..23 of the first unit
 #endif
@@ -149,7 +153,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
   // softmax warpgroups get the rest of the CTA's launch allocation (168 x 384 = 64512 =
   // 56*128 + 224*256; setmaxnreg only redistributes the CTA's own registers).
   if (warp < 4) {
-  ptx::setmaxnreg_dec<56>();
+  ptx::setmaxnreg_dec<DN_REG_CTL>();
   if (warp == 0) {
     // ===================== TMA producer: 64-key K/V blocks into the stage ring =====================
     // The entries of the next block (and the next unit's header) are loaded one step
@@ -350,7 +354,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
     }
   }
   } else {
-    ptx::setmaxnreg_inc<224>();
+    ptx::setmaxnreg_inc<DN_REG_SM>();
     // ===================== softmax / epilogue (tile t) =====================
     const int t = (warp - 4) >> 2;                    // 0 = tile A, 1 = tile B
     const int r = threadIdx.x - 128 - 128 * t;        // row within the tile = TMEM lane
