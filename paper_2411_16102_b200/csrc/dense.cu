@@ -94,7 +94,10 @@ __device__ __forceinline__ int snake_unit(int k) {
 }
 
 // POLY: bit k set -> pair k (of 16 per 32-key chunk) takes the FMA-pipe polynomial exp2
-template <int D, int BOX, uint32_t POLY = 0x8888u>
+#ifndef DN_POLY_MASK
+#define DN_POLY_MASK 0x8888u   // pairs on the FMA-pipe polynomial: 4 of 16
+#endif
+template <int D, int BOX, uint32_t POLY = DN_POLY_MASK>
 __global__ void __launch_bounds__(DN_THREADS, 1)
     dense_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
                  const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmq1,
@@ -368,15 +371,18 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
     long long cu_prev_end = 0;
 #endif
     uint32_t scnt0 = 0, scnt1 = 0;                    // s_full completions consumed per S buffer (registers)
-    int2 enext[EPB];                                  // {pos0, count} of the next block's entries
+    // {pos0, count} of the next block's entries, as loaded, and whether each is padding: the
+    // padding select is applied when the block is processed, so no instruction waits on
+    // the load right after issuing it
+    int2 enext[EPB];
+    bool epad[EPB];
     auto load_meta = [&](const Unit& un, int j) {
 #pragma unroll
       for (int i = 0; i < EPB; ++i) {   // one 8-byte load per entry, no branch (padding: count 0)
         const int e = un.entry_begin + j * EPB + i;
         const int ec = e < un.entry_end ? e : un.entry_end - 1;
-        int2 v = *reinterpret_cast<const int2*>(&p.entries[ec].pos0);
-        if (e >= un.entry_end) v.y = 0;
-        enext[i] = v;
+        enext[i] = *reinterpret_cast<const int2*>(&p.entries[ec].pos0);
+        epad[i] = e >= un.entry_end;
       }
     };
     for (int uk = 0, ui = snake_unit(0); ui < p.n_units; ui = snake_unit(++uk)) {
@@ -415,7 +421,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         // this block's {pos0, count} were loaded one block ahead (latency off the critical path)
         int2 ecur[EPB];
 #pragma unroll
-        for (int i = 0; i < EPB; ++i) ecur[i] = enext[i];
+        for (int i = 0; i < EPB; ++i) ecur[i] = make_int2(enext[i].x, epad[i] ? 0 : enext[i].y);
         if (j + 1 < nb) load_meta(u, j + 1);
         int vis[EPB];
         bool full_vis = true;

@@ -1,36 +1,54 @@
-// dense_ks.cu — the dense pass for key-split units (tcgen05 + TMEM + TMA).
+// dense.cu — the dense pass on the 5th-gen tensor cores (tcgen05 + TMEM + TMA).
 //
-// A dense unit with at most 128 query rows (a short prefill chunk, or a chunk's last
-// rows) fills one 128-row Q tile; run like the two-tile units of dense.cu it would
-// leave the second tile of the CTA idle and its tensor / softmax pipeline without a
-// ping-pong partner (measured: ~1,670 cycles per 64-key block against ~1,880 for a block
-// of two tiles, i.e. 86 % of the time for half the work).  Here both tiles serve the
-// unit's rows: tile t takes the 64-key blocks j = t (mod 2) — both read the one Q tile —
-// and the two partial results are merged by log-sum-exp at the epilogue (the
-// same identity the LSE-merge pass uses):
-//   O = (2^(mA-m) O_A + 2^(mB-m) O_B) / (2^(mA-m) lA + 2^(mB-m) lB),  m = max(mA, mB).
-// K and V have separate rings (a K slot frees as soon as its QK is done), so the QK of
-// a tile's next-but-one block (4 blocks ahead) never waits for its K.  The kernel is a
-// separate launch (a PDL dependent of the streaming grid) so that dense.cu's two-tile
-// kernel keeps its own code generation.  Warp roles, TMEM map and the softmax are those
-// of dense.cu.
+// Work units with many rows per kv head — a SEPARATE shared-prefix node attended
+// once by all the SMALL requests under it (PAPER §5 P:11 "exactly-once computation
+// of shared prefixes"; §7.2 P:248-251 cascade reuse of the shared KV access), or a
+// BIG request (chunked prefill) — are dense contractions: up to 256 query
+// rows (tokens x grouped q heads) against 64-key blocks of the node's pages.
+//
+// One persistent CTA per SM, warp-specialised, two 128-row Q tiles (A, B) that
+// share every K/V block ("ping-pong": the tensor pipe works on one tile while the
+// other tile's softmax runs):
+//   warp 0       TMA producer: 64-key K/V blocks (page entries, 128B swizzle) into a
+//                4-stage smem ring
+//   warp 1       MMA issuer (whole warp, one elected lane issues): S_t = Q_t K^T (UMMA
+//                128x64x16, K-major A/B) into one of two TMEM S buffers per tile;
+//                O_t += P_t V with P_t read from TMEM (aliasing its S buffer) and V
+//                MN-major from smem; tcgen05.commit -> mbarriers
+//   warp 2       TMEM allocator (512 columns: S_A0 S_A1 | S_B0 S_B1 | O_A | O_B)
+//   warp 3       Q loader: the next unit's Q tiles as soon as the current unit's last
+//                QK has been issued — 3-D TMA boxes {64, g, 128/g} when the unit's
+//                tokens are consecutive rows of q, one box per token otherwise,
+//                cp.async row gathers when g does not divide 128
+//   warps 4..7   softmax / epilogue of tile A, warps 8..11 of tile B: thread =
+//                query row = TMEM lane; tcgen05.ld the S row, per-row causal mask,
+//                log2-domain online softmax with lazy O rescaling (only when the
+//                running max grows by > 2^8; blocks whose exponentials sum to <= 2^8
+//                against the running reference skip the block max), exp2 3/4 on
+//                MUFU and 1/4 as an FMA-pipe polynomial, P -> bf16 -> tcgen05.st,
+//                final O / l through a per-warp smem staging tile with coalesced
+//                row-segment stores (bf16 output rows or fp32 partial rows).
+// MMAs of one thread execute in issue order, so QK_t(j+2) (which overwrites the S
+// buffer holding P_t(j)) is issued right after PV_t(j) without a further barrier.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <string.h>
+
+#include <type_traits>
 
 #include "blend.h"
 #include "common.cuh"
 #include "ptx.cuh"
 
 namespace blend {
-namespace ks {
 
-#ifndef DN_KS_NSTAGE128
-#define DN_KS_NSTAGE128 5  // K / V ring slots at D = 128 (64 keys each)
-#endif
 #ifndef DN_NSTAGE128
-#define DN_NSTAGE128 4
+#define DN_NSTAGE128 4     // K/V ring stages at D = 128 (64 keys each)
+#endif
+#ifndef DN_REG_CTL
+#define DN_REG_CTL 56      // setmaxnreg of warpgroup 0 (producer, MMA, allocator, Q loader)
+#define DN_REG_SM 224      // setmaxnreg of the softmax warpgroups (56*128 + 224*256 = 64512)
 #endif
 #ifndef BLEND_TRACE_WARPS
 #define BLEND_TRACE_WARPS 0    // 1: per-warp P hand-off stamps for blocks 20..23 of the first unit
@@ -50,7 +68,7 @@ constexpr uint32_t DN_TMEM_COLS = 512;
 constexpr float DN_RESCALE_T = 8.0f;     // lazy-rescale threshold (log2 units)
 
 struct DenseSmem {
-  uint32_t q0, q1, k0, v0, slot, bar, stg, total;
+  uint32_t q0, q1, stage0, stage_stride, bar, stg, total;
   int nstage;
 };
 
@@ -58,12 +76,11 @@ __host__ __device__ inline DenseSmem dense_layout(int D) {
   DenseSmem L;
   const int CH = D / 64;
   L.q0 = 0;
-  L.q1 = 0;                              // one Q tile only (both tiles read it)
-  L.slot = CH * DN_KCHUNK;               // one 64-key K (or V) block
-  L.nstage = D == 128 ? DN_KS_NSTAGE128 : 8;   // the second Q tile's space holds an extra K and V slot
-  L.k0 = CH * DN_QCHUNK;                 // K ring, then V ring (a K slot frees at QK, a V slot at PV)
-  L.v0 = L.k0 + L.nstage * L.slot;
-  L.bar = L.v0 + L.nstage * L.slot;
+  L.q1 = CH * DN_QCHUNK;
+  L.stage0 = 2 * CH * DN_QCHUNK;
+  L.stage_stride = 2 * CH * DN_KCHUNK;   // K chunks then V chunks
+  L.nstage = D == 128 ? DN_NSTAGE128 : 8;
+  L.bar = L.stage0 + L.nstage * L.stage_stride;
   L.stg = L.bar + 512;                    // epilogue staging: per softmax warp 32 rows x 128 B
   L.total = L.stg + 8 * 4096;
   return L;
@@ -84,7 +101,7 @@ __device__ __forceinline__ int snake_unit(int k) {
 #endif
 template <int D, int BOX, uint32_t POLY = DN_POLY_MASK>
 __global__ void __launch_bounds__(DN_THREADS, 1)
-    dense_ks_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
+    dense_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
                  const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmq1,
                  AttnParams p) {
   constexpr int CH = D / 64;
@@ -94,26 +111,31 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
   const DenseSmem L = dense_layout(D);
   const int NS = L.nstage;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar);
-  uint64_t* k_full = bars;             // [NS <= 8]
-  uint64_t* k_empty = bars + 8;        // [NS]: every QK that reads the K slot issued (and done)
-  uint64_t* v_full = bars + 16;        // [NS]
-  uint64_t* v_empty = bars + 24;       // [NS]: every PV that reads the V slot done
-  uint64_t* s_full = bars + 32;        // [tile][buffer]
-  uint64_t* p_full = bars + 36;        // [tile][buffer]
-  uint64_t* o_done = bars + 40;        // [tile][buffer]: PV of a block that used this S buffer
-  uint64_t* q_full = bars + 44;
-  uint64_t* q_empty = bars + 45;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 46);
+  uint64_t* kv_full = bars;            // [NS <= 8]
+  uint64_t* kv_empty = bars + 8;       // [NS]
+  uint64_t* s_full = bars + 16;        // [tile][buffer]
+  uint64_t* p_full = bars + 20;        // [tile][buffer]
+  uint64_t* o_done = bars + 24;        // [tile][buffer]: PV of a block that used this S buffer
+  uint64_t* q_full = bars + 28;
+  uint64_t* q_empty = bars + 29;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 30);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) trace_stamp(p, 0);
-  ptx::pdl_launch_dependents();   // the merge grid may be scheduled (it waits for this grid first)
+  if (p.sched != nullptr && blockIdx.x == 0) {
+    // reset the streaming pass's unit counter before this CTA's launch trigger: the
+    // dependent (streaming) grid cannot start before every CTA of this grid has triggered
+    if (threadIdx.x == 0) {
+      if (atomicExch(p.sched, 0) == 0x7fffffff) __trap();   // consumes the result: the exchange has completed
+      __threadfence();
+    }
+    __syncthreads();
+  }
+  ptx::pdl_launch_dependents();   // the streaming pass may start on SMs this grid leaves free
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
-      ptx::mbar_init(&k_full[s], 1);
-      ptx::mbar_init(&k_empty[s], 1);
-      ptx::mbar_init(&v_full[s], 1);
-      ptx::mbar_init(&v_empty[s], 1);
+      ptx::mbar_init(&kv_full[s], 1);
+      ptx::mbar_init(&kv_empty[s], 1);
     }
     for (int i = 0; i < 4; ++i) {
       ptx::mbar_init(&s_full[i], 1);
@@ -136,14 +158,11 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
   // softmax warpgroups get the rest of the CTA's launch allocation (168 x 384 = 64512 =
   // 56*128 + 224*256; setmaxnreg only redistributes the CTA's own registers).
   if (warp < 4) {
-  ptx::setmaxnreg_dec<56>();
+  ptx::setmaxnreg_dec<DN_REG_CTL>();
   if (warp == 0) {
-    // ===================== TMA producer: 64-key K blocks and V blocks into their rings =====================
-    // The CTA's blocks form one stream b = 0, 1, ...; the loop issues K(b) and then V(b-1),
-    // so a K block (needed by the next QK) never waits behind a V slot (freed only by the
-    // PV two blocks later).  The entries of the next block (and the next unit's header)
-    // are loaded one step ahead, so a freed slot is refilled without waiting on dependent
-    // global loads.
+    // ===================== TMA producer: 64-key K/V blocks into the stage ring =====================
+    // The entries of the next block (and the next unit's header) are loaded one step
+    // ahead, so a freed stage is refilled without waiting on dependent global loads.
     if (lane == 0) {
       ptx::tma_prefetch_desc(&tmk);
       ptx::tma_prefetch_desc(&tmv);
@@ -152,7 +171,6 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       int uk = 0, ui = snake_unit(0);
       Unit u = ui < p.n_units ? p.units[ui] : Unit{};
       int4 cur[EPB];
-      int32_t yprev[EPB];   // TMA rows of block kit-1 (its V is issued after K(kit))
       auto load_block = [&](const Unit& un, int j) {
 #pragma unroll
         for (int i = 0; i < EPB; ++i) {
@@ -163,16 +181,6 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
           if (pad) cur[i].w = 0;
         }
       };
-      auto issue_v = [&](uint32_t b) {
-        const uint32_t s = b % NS, ph = (b / NS) & 1;
-        ptx::mbar_wait(&v_empty[s], ph ^ 1);
-        uint8_t* vst = smem + L.v0 + s * L.slot;
-        ptx::mbar_arrive_expect_tx(&v_full[s], (uint32_t)(CH * DN_KCHUNK));
-#pragma unroll
-        for (int i = 0; i < EPB; ++i)
-#pragma unroll
-          for (int c = 0; c < CH; ++c) ptx::tma_load_2d(vst + c * DN_KCHUNK + i * BOX * 128, &tmv, &v_full[s], c * 64, yprev[i]);
-      };
       if (ui < p.n_units) load_block(u, 0);
       while (ui < p.n_units) {
         const int nb = (u.entry_end - u.entry_begin + EPB - 1) / EPB;
@@ -180,27 +188,26 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         const Unit un = ui_next < p.n_units ? p.units[ui_next] : Unit{};
         for (int j = 0; j < nb; ++j, ++kit) {
           const uint32_t s = kit % NS, ph = (kit / NS) & 1;
-          ptx::mbar_wait(&k_empty[s], ph ^ 1);
-          uint8_t* kst = smem + L.k0 + s * L.slot;
+          ptx::mbar_wait(&kv_empty[s], ph ^ 1);
+          uint8_t* kst = smem + L.stage0 + s * L.stage_stride;
+          uint8_t* vst = kst + CH * DN_KCHUNK;
           if (kit == 0) trace_stamp(p, 3);
-          ptx::mbar_arrive_expect_tx(&k_full[s], (uint32_t)(CH * DN_KCHUNK));
-          int32_t y[EPB];
+          ptx::mbar_arrive_expect_tx(&kv_full[s], 2u * CH * DN_KCHUNK);
 #pragma unroll
           for (int i = 0; i < EPB; ++i) {
-            y[i] = (cur[i].x * p.hkv + u.kvh) * p.ps + cur[i].y;   // {page, row_off, pos0, count}
+            const int32_t y = (cur[i].x * p.hkv + u.kvh) * p.ps + cur[i].y;   // {page, row_off, pos0, count}
 #pragma unroll
-            for (int c = 0; c < CH; ++c) ptx::tma_load_2d(kst + c * DN_KCHUNK + i * BOX * 128, &tmk, &k_full[s], c * 64, y[i]);
+            for (int c = 0; c < CH; ++c) {
+              ptx::tma_load_2d(kst + c * DN_KCHUNK + i * BOX * 128, &tmk, &kv_full[s], c * 64, y);
+              ptx::tma_load_2d(vst + c * DN_KCHUNK + i * BOX * 128, &tmv, &kv_full[s], c * 64, y);
+            }
           }
-          if (kit > 0) issue_v(kit - 1);
-#pragma unroll
-          for (int i = 0; i < EPB; ++i) yprev[i] = y[i];
           if (j + 1 < nb) load_block(u, j + 1);
           else if (ui_next < p.n_units) load_block(un, 0);
         }
         ui = ui_next;
         u = un;
       }
-      if (kit > 0) issue_v(kit - 1);
     }
   } else if (warp == 3) {
     // ===================== Q loader: next unit's rows as soon as its last QK is issued =====
@@ -292,68 +299,59 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       // lo = start address >> 4 | LBO >> 4 << 16, advanced by immediates
       const uint64_t qd0 = ptx::umma_desc_sw128(ptx::smem_u32(smem + L.q0), 16, 1024);
       const uint32_t q_lo0 = (uint32_t)qd0, q_hi = (uint32_t)(qd0 >> 32);
-      const uint64_t kd0 = ptx::umma_desc_sw128(ptx::smem_u32(smem + L.k0), 16, 1024);
+      const uint32_t q_lo1 = (uint32_t)ptx::umma_desc_sw128(ptx::smem_u32(smem + L.q1), 16, 1024);
+      const uint64_t kd0 = ptx::umma_desc_sw128(ptx::smem_u32(smem + L.stage0), 16, 1024);
       const uint32_t k_lo0 = (uint32_t)kd0, k_hi = (uint32_t)(kd0 >> 32);
-      const uint64_t vd0 = ptx::umma_desc_sw128(ptx::smem_u32(smem + L.v0), DN_KCHUNK, 1024);
+      const uint64_t vd0 = ptx::umma_desc_sw128(ptx::smem_u32(smem + L.stage0 + CH * DN_KCHUNK), DN_KCHUNK, 1024);
       const uint32_t v_lo0 = (uint32_t)vd0, v_hi = (uint32_t)(vd0 >> 32);
-      const uint32_t stage_lo = L.slot >> 4;
+      const uint32_t stage_lo = L.stage_stride >> 4;
       const uint32_t leader = ptx::elect_one();
       uint32_t kit = 0, gu = 0;
       uint32_t pbits = 0;               // parity of the next p_full[tile][buffer] completion (bit pi)
       for (int uk = 0, ui = snake_unit(0); ui < p.n_units; ui = snake_unit(++uk)) {
         const Unit u = p.units[ui];
         const int nb = (u.entry_end - u.entry_begin + EPB - 1) / EPB;
-        auto wait_k = [&](int j) {
-          ptx::mbar_wait(&k_full[(kit + j) % NS], ((kit + j) / NS) & 1);
+        const int ntile = u.n_rows > 128 ? 2 : 1;
+        auto wait_kv = [&](int j) {
+          ptx::mbar_wait(&kv_full[(kit + j) % NS], ((kit + j) / NS) & 1);
           ptx::tc_fence_after();
         };
-        auto wait_v = [&](int j) {
-          ptx::mbar_wait(&v_full[(kit + j) % NS], ((kit + j) / NS) & 1);
-          ptx::tc_fence_after();
+        auto issue_qk = [&](int t, int j) {
+          const uint32_t qlo = t ? q_lo1 : q_lo0;
+          const uint32_t klo = k_lo0 + ((kit + j) % NS) * stage_lo;
+          const uint32_t dcol = tmem + t * 128 + (j & 1) * DN_KB;
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk)
+            ptx::umma_ss_lohi(leader, dcol, qlo + (((kk / 4) * DN_QCHUNK + (kk % 4) * 32) >> 4), q_hi,
+                              klo + (((kk / 4) * DN_KCHUNK + (kk % 4) * 32) >> 4), k_hi, IDESC_QK, kk > 0);
+          ptx::umma_commit_if(leader, &s_full[t * 2 + (j & 1)]);
         };
         ptx::mbar_wait(q_full, gu & 1);
         ptx::tc_fence_after();
         if (gu == 0 && lane == 0) trace_stamp(p, 2);
-        {
-          // tile t takes the blocks j = t (mod 2) of the one Q
-          // tile (both read Q tile A), local block i = j / 2 in its S buffer i & 1, so the two
-          // tiles ping-pong over one K/V stream; the softmax merges their partial O at the
-          // end.  QK(j+4) is issued after PV(j) (the tile's next-but-one block); its K slot
-          // was freed by QK(j).
-          auto issue_qk_ks = [&](int j) {
-            const int t = j & 1, b = (j >> 1) & 1;
-            const uint32_t klo = k_lo0 + ((kit + j) % NS) * stage_lo;
-#pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk)
-              ptx::umma_ss_lohi(leader, tmem + t * 128 + b * DN_KB, q_lo0 + (((kk / 4) * DN_QCHUNK + (kk % 4) * 32) >> 4),
-                                q_hi, klo + (((kk / 4) * DN_KCHUNK + (kk % 4) * 32) >> 4), k_hi, IDESC_QK, kk > 0);
-            ptx::umma_commit_if(leader, &s_full[t * 2 + b]);
-            ptx::umma_commit_if(leader, &k_empty[(kit + j) % NS]);
-          };
-          for (int j = 0; j < 4 && j < nb; ++j) {
-            wait_k(j);
-            issue_qk_ks(j);
-          }
-          if (nb <= 4) ptx::umma_commit_if(leader, q_empty);
-          for (int j = 0; j < nb; ++j) {
-            const int t = j & 1, b = (j >> 1) & 1, pi = t * 2 + b;
-            wait_v(j);
+        for (int j = 0; j < 2 && j < nb; ++j) {
+          wait_kv(j);
+          for (int t = 0; t < ntile; ++t) issue_qk(t, j);
+        }
+        if (nb <= 2) ptx::umma_commit_if(leader, q_empty);   // every QK of the unit issued: Q may be reloaded
+        for (int j = 0; j < nb; ++j) {
+          const uint32_t vlo = v_lo0 + ((kit + j) % NS) * stage_lo;
+          if (j + 2 < nb) wait_kv(j + 2);
+          for (int t = 0; t < ntile; ++t) {
+            const int pi = t * 2 + (j & 1);
             ptx::mbar_wait(&p_full[pi], (pbits >> pi) & 1);
             pbits ^= 1u << pi;
             ptx::tc_fence_after();
-            const uint32_t vlo = v_lo0 + ((kit + j) % NS) * stage_lo;
+            const uint32_t acol = tmem + t * 128 + (j & 1) * DN_KB;
 #pragma unroll
             for (int kk = 0; kk < DN_KB / 16; ++kk)
-              ptx::umma_ts_lohi(leader, tmem + 256 + t * D, tmem + t * 128 + b * DN_KB + kk * 8,
-                                vlo + ((kk * 16 * 128) >> 4), v_hi, IDESC_PV, (j > 1 || kk > 0) ? 1u : 0u);
+              ptx::umma_ts_lohi(leader, tmem + 256 + t * D, acol + kk * 8, vlo + ((kk * 16 * 128) >> 4), v_hi,
+                                IDESC_PV, (j > 0 || kk > 0) ? 1u : 0u);
             ptx::umma_commit_if(leader, &o_done[pi]);
-            if (j + 4 < nb) {
-              wait_k(j + 4);
-              issue_qk_ks(j + 4);
-            }
-            if (j + 5 == nb) ptx::umma_commit_if(leader, q_empty);   // QK(nb-1) issued
-            ptx::umma_commit_if(leader, &v_empty[(kit + j) % NS]);
+            if (j + 2 < nb) issue_qk(t, j + 2);
           }
+          if (j + 3 == nb) ptx::umma_commit_if(leader, q_empty);   // QK(nb-1) of every tile issued
+          ptx::umma_commit_if(leader, &kv_empty[(kit + j) % NS]);
         }
         kit += nb;
         ++gu;
@@ -361,12 +359,13 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
     }
   }
   } else {
-    ptx::setmaxnreg_inc<224>();
+    ptx::setmaxnreg_inc<DN_REG_SM>();
     // ===================== softmax / epilogue (tile t) =====================
     const int t = (warp - 4) >> 2;                    // 0 = tile A, 1 = tile B
     const int r = threadIdx.x - 128 - 128 * t;        // row within the tile = TMEM lane
     const uint32_t lane_base = (uint32_t)(((warp - 4) & 3) * 32) << 16;
     const uint32_t col_o = 256 + t * D;
+    uint32_t sb = 0;                                  // blocks of this tile processed so far
 #if BLEND_TRACE_UNITS
     long long ph_acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};   // per fast block: two-tile [4], single-tile [4], counts [2]
     long long cu_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // clock64 sums: start->S0, S0->last P, epilogue, gap; blocks; units;
@@ -376,7 +375,8 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
     uint32_t scnt0 = 0, scnt1 = 0;                    // s_full completions consumed per S buffer (registers)
     // {pos0, count} of the next block's entries, as loaded, and whether each is padding: the
     // padding select is applied when the block is processed, so no instruction waits on
-    // the load right after issuing it
+    // the load right after issuing it (a select on the loaded value stalled each block
+    // for a full L2 round trip ahead of its S wait)
     int2 enext[EPB];
     bool epad[EPB];
     auto load_meta = [&](const Unit& un, int j) {
@@ -388,13 +388,116 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         epad[i] = e >= un.entry_end;
       }
     };
-    uint32_t sbase = 0;                               // stream index of the unit's first block (K / V slots)
+    // Deferred epilogue: a unit's O is read from TMEM during the tile's NEXT unit, after that
+    // unit's first P is in TMEM and before its hand-off (the PV of that block overwrites O),
+    // and normalised / stored right after the hand-off.  So the next unit's metadata loads,
+    // its first S and first softmax block overlap the last PVs of the unit, and the stores
+    // overlap the next unit's first PV and QK, instead of the tensor pipe idling through a
+    // serial epilogue at every unit boundary.  ep_* describe the pending unit's rows.
+    bool ep_pending = false;
+    int32_t ep_tgt = PM_SKIP, ep_token = 0, ep_head = 0;
+    float ep_m = -INFINITY, ep_l = 0.f;
+    uint32_t ep_bar = 0, ep_par = 0;                  // o_done barrier of its last PV, and its parity
+    // wait for the pending unit's last PV (MMAs complete in issue order, so this certifies
+    // every earlier PV of the unit) and read its O row
+    auto ep_read = [&](uint32_t (&ov)[D]) {
+      ptx::mbar_wait(&o_done[ep_bar], ep_par);
+      ptx::tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) ptx::tmem_ld32(tmem + lane_base + col_o + c * 32, ov + 32 * c);
+      ptx::tmem_wait_ld();
+    };
+    // O / l leaves through a per-warp smem staging tile (XOR-swizzled 16-B units, no bank
+    // conflicts), so that every global store instruction writes whole row segments of 4
+    // rows instead of 32 scattered pieces.  Row kinds: 2 = fp32 partial row, 1 = bf16 output
+    // row (DIRECT), 0 = nothing.  A warp whose rows are all bf16 outputs (or nothing) stages
+    // 64 columns as bf16 per pass (one 128-B line per row: every STG.128 writes 4 whole
+    // lines); a warp with partial rows stages 32 fp32 columns per pass.
+    auto ep_store = [&](const uint32_t (&ov)[D]) {
+      const float m_use = ep_m == -INFINITY ? 0.f : ep_m;
+      const float inv = ep_l > 0.f ? 1.f / ep_l : 0.f;
+      const float lse2 = ep_l > 0.f ? m_use + log2f(ep_l) : -INFINITY;
+      const int kind = ep_tgt == PM_DIRECT ? 1 : (ep_tgt >= 0 ? 2 : 0);
+      char* rowp = kind == 1 ? reinterpret_cast<char*>(p.out) + ((int64_t)ep_token * p.hq + ep_head) * D * 2
+                 : kind == 2 ? reinterpret_cast<char*>(p.ws_o + ((int64_t)ep_tgt * p.hq + ep_head) * D) : nullptr;
+      const uint32_t stg = ptx::smem_u32(smem + L.stg + (warp - 4) * 4096);
+      const int k8 = lane & 7;
+      char* rp[8];
+      int rk[8];
+#pragma unroll
+      for (int s_ = 0; s_ < 8; ++s_) {          // rows s_ * 4 + lane / 8 of this warp, for the copy-out
+        const int rr = s_ * 4 + (lane >> 3);
+        rp[s_] = reinterpret_cast<char*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(rowp), rr));
+        rk[s_] = __shfl_sync(0xffffffffu, kind, rr);
+      }
+      const bool all_bf16 = __all_sync(0xffffffffu, kind != 2);
+      if (all_bf16) {
+#pragma unroll
+        for (int hh = 0; hh < D / 64; ++hh) {
+#pragma unroll
+          for (int u8 = 0; u8 < 8; ++u8) {
+            const uint32_t* o8 = ov + hh * 64 + 8 * u8;
+            ptx::sts128u(stg + ptx::sw128(lane, u8),
+                         ptx::pack_bf16(__uint_as_float(o8[0]) * inv, __uint_as_float(o8[1]) * inv),
+                         ptx::pack_bf16(__uint_as_float(o8[2]) * inv, __uint_as_float(o8[3]) * inv),
+                         ptx::pack_bf16(__uint_as_float(o8[4]) * inv, __uint_as_float(o8[5]) * inv),
+                         ptx::pack_bf16(__uint_as_float(o8[6]) * inv, __uint_as_float(o8[7]) * inv));
+          }
+          __syncwarp();
+          uint4 v[8];   // all eight row segments in flight before the first store
+#pragma unroll
+          for (int s_ = 0; s_ < 8; ++s_) v[s_] = ptx::lds128u(stg + ptx::sw128(s_ * 4 + (lane >> 3), k8));
+#pragma unroll
+          for (int s_ = 0; s_ < 8; ++s_)
+            if (rk[s_] == 1) ptx::stg128u(rp[s_] + hh * 128 + k8 * 16, v[s_]);
+          __syncwarp();   // the staging tile is rewritten by the next chunk
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          const uint32_t* o32 = ov + 32 * c;
+#pragma unroll
+          for (int u8 = 0; u8 < 8; ++u8)
+            ptx::sts128(stg + ptx::sw128(lane, u8), __uint_as_float(o32[4 * u8]) * inv,
+                        __uint_as_float(o32[4 * u8 + 1]) * inv, __uint_as_float(o32[4 * u8 + 2]) * inv,
+                        __uint_as_float(o32[4 * u8 + 3]) * inv);
+          __syncwarp();
+          float4 v[8];   // all eight row segments in flight before the first store
+#pragma unroll
+          for (int s_ = 0; s_ < 8; ++s_) v[s_] = ptx::lds128(stg + ptx::sw128(s_ * 4 + (lane >> 3), k8));
+#pragma unroll
+          for (int s_ = 0; s_ < 8; ++s_) {
+            if (rk[s_] == 2)
+              ptx::stg128(rp[s_] + c * 128 + k8 * 16, v[s_]);
+            else if (rk[s_] == 1)
+              ptx::stg64(rp[s_] + c * 64 + k8 * 8, ptx::pack_bf16(v[s_].x, v[s_].y), ptx::pack_bf16(v[s_].z, v[s_].w));
+          }
+          __syncwarp();   // the staging tile is rewritten by the next chunk
+        }
+      }
+      if (ep_tgt == PM_DIRECT) p.lse[(int64_t)ep_token * p.hq + ep_head] = lse2 * kLn2;
+      else if (ep_tgt >= 0) p.ws_lse[(int64_t)ep_tgt * p.hq + ep_head] = lse2;
+    };
+    // P hand-off of block j; in a unit's first block the pending epilogue's O is read first
+    auto hand_off = [&](const bool first, int buf) __attribute__((always_inline)) {
+      if (first && ep_pending) {
+        uint32_t ov[D];
+        ep_read(ov);
+        ptx::tc_fence_before();   // the O reads are ordered before the hand-off (PV(0) overwrites O)
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&p_full[t * 2 + buf]);
+        ep_store(ov);
+        ep_pending = false;
+      } else {
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&p_full[t * 2 + buf]);
+      }
+    };
     for (int uk = 0, ui = snake_unit(0); ui < p.n_units; ui = snake_unit(++uk)) {
       const Unit u = p.units[ui];
       const int nb = (u.entry_end - u.entry_begin + EPB - 1) / EPB;
-      // both tiles serve the unit's rows, tile t the blocks j = t (mod 2); the partial
-      // results are merged at the epilogue
-      const int row = r;                              // row within the unit
+      if (t == 1 && u.n_rows <= 128) continue;       // tile B idle for this unit
+      const int row = 128 * t + r;                    // row within the unit
 #if BLEND_TRACE_UNITS
       if (threadIdx.x == 128 && uk < 10) trace_stamp(p, 20 + 4 * uk);
       const long long cu0 = clock64();
@@ -417,17 +520,20 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       // softmax: its P rows only feed its own (never stored) O rows, so they may hold
       // anything; it keeps the barrier protocol
       const bool warp_pad = __all_sync(0xffffffffu, !row_ok);
-      int nloc = 0;                                   // blocks this tile processes in this unit
-      load_meta(u, t);
-      for (int j = t; j < nb; j += 2, ++nloc) {
-        const int buf = nloc & 1;
+      load_meta(u, 0);
+      // block j of the unit; FIRST (block 0, peeled) also carries the previous unit's deferred
+      // epilogue, so the hot loop (blocks 1..) keeps none of its state live
+      auto block = [&](const int j, auto first_tag) __attribute__((always_inline)) {
+        constexpr bool FIRST = decltype(first_tag)::value;
+        const int buf = j & 1;
         const uint32_t col_s = t * 128 + buf * DN_KB;
-        const uint32_t sb = sbase + j;                // stream index of block j (its K / V slot)
+        // key positions of this block from the stage metadata the producer wrote (the
+        // stage cannot be refilled before this block's P is consumed)
         // this block's {pos0, count} were loaded one block ahead (latency off the critical path)
         int2 ecur[EPB];
 #pragma unroll
         for (int i = 0; i < EPB; ++i) ecur[i] = make_int2(enext[i].x, epad[i] ? 0 : enext[i].y);
-        if (j + 2 < nb) load_meta(u, j + 2);
+        if (j + 1 < nb) load_meta(u, j + 1);
         int vis[EPB];
         bool full_vis = true;
 #pragma unroll
@@ -453,15 +559,13 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         // Entries with count < BOX (a node's last page, padding entries): their V rows past
         // the count may hold anything, NaN included, and the PV MMA would multiply them by
         // P = 0 -> tile A's warpgroup zeroes them before its P hand-off (the PV MMAs of both
-        // tiles are issued after it; in a key-split unit each tile zeroes its own blocks).
-        // K rows past the count only reach masked scores.
-        {
+        // tiles are issued after it).  K rows past the count only reach masked scores.
+        if (t == 0) {
           bool part = false;
 #pragma unroll
           for (int i = 0; i < EPB; ++i) part = part || ecur[i].y < BOX;
           if (part) {
-            ptx::mbar_wait(&v_full[sb % NS], (sb / NS) & 1);   // V(j) has landed (K and V arrive separately)
-            uint8_t* vst = smem + L.v0 + (sb % NS) * L.slot;
+            uint8_t* vst = smem + L.stage0 + (sb % NS) * L.stage_stride + CH * DN_KCHUNK;
 #pragma unroll
             for (int i = 0; i < EPB; ++i) {
               const int nz = BOX - ecur[i].y;
@@ -479,9 +583,8 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         if (threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 8 + 2 * j);
 #endif
         if (warp_pad) {
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&p_full[t * 2 + buf]);
-          continue;
+          hand_off(FIRST, buf);
+          return;
         }
         float sv[DN_KB];
         ptx::tmem_ld32(tmem + lane_base + col_s, reinterpret_cast<uint32_t*>(sv));
@@ -540,7 +643,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         if (p.stats != nullptr && lane == 0) {   // diagnostics: blocks per softmax path
           stat_add(p, STAT_DENSE_BLOCKS, 1);
           if (slow) stat_add(p, STAT_DENSE_SLOW, 1);
-          if (slow && nloc > 0) stat_add(p, STAT_DENSE_SLOW_LATE, 1);
+          if (slow && j > 0) stat_add(p, STAT_DENSE_SLOW_LATE, 1);
         }
         if (slow) {
         float mxv[8];
@@ -552,12 +655,12 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
                                fmaxf(fmaxf(mxv[4], mxv[5]), fmaxf(mxv[6], mxv[7])));
         const float mx2 = mx * p.scale_log2;
         const bool need = mx2 > m_ref + DN_RESCALE_T;
-        if (nloc > 0 && __any_sync(0xffffffffu, need)) {
+        if (j > 0 && __any_sync(0xffffffffu, need)) {
           if (lane == 0) stat_add(p, STAT_DENSE_RESCALE, 1);
           // O holds PV up to block j-1: wait for it.  Parity is unambiguous because the
           // previous completion on this barrier (PV(j-3)) is certified by s_full(j-1) and
           // PV(j+1) cannot be issued before this block's P.
-          const int pb_ = (nloc - 1) & 1;
+          const int pb_ = (j - 1) & 1;
           ptx::mbar_wait(&o_done[t * 2 + pb_], ((pb_ ? scnt1 : scnt0) - 1) & 1);
           ptx::tc_fence_after();
           const float alpha = need ? ptx::ex2(m_ref - mx2) : 1.f;
@@ -582,8 +685,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
         l += lsum;
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&p_full[t * 2 + buf]);
+        hand_off(FIRST, buf);
 #if BLEND_TRACE_UNITS
         if (threadIdx.x == 128 && !slow) {
           const long long ph5 = clock64();
@@ -601,7 +703,10 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
 #if BLEND_TRACE_BLOCKS
         if (threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 9 + 2 * j);
 #endif
-      }
+      };
+      block(0, std::true_type{});
+      ++sb;
+      for (int j = 1; j < nb; ++j, ++sb) block(j, std::false_type{});
       if (threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 4);
 #if BLEND_TRACE_UNITS
       if (threadIdx.x == 128 && uk < 10) trace_stamp(p, 22 + 4 * uk);
@@ -615,146 +720,28 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
       }
       cu_acc[5] += 1;
 #endif
-      // ---- epilogue: PV of the unit's last block done (MMAs complete in issue order, so
-      // this also certifies every earlier PV of the unit)
+      // ---- epilogue, deferred to the tile's next unit (or the end of the CTA's units)
       {
-        const int lb = (nloc - 1) & 1;
-        ptx::mbar_wait(&o_done[t * 2 + lb], ((lb ? scnt1 : scnt0) - 1) & 1);
+        const int lb = (nb - 1) & 1;
+        ep_bar = t * 2 + lb;
+        ep_par = ((lb ? scnt1 : scnt0) - 1) & 1;
+        ep_tgt = tgt;
+        ep_token = token;
+        ep_head = head;
+        ep_m = m_ref;
+        ep_l = l;
+        ep_pending = true;
       }
-      ptx::tc_fence_after();
-      if (threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 60);
-      // Key-split unit: tile B hands its row state (m, l) to tile A through its staging
-      // tile (named barrier per lane quarter, 64 threads) and waits until tile A has read
-      // O_B out of TMEM; tile A merges the two partials: O = (2^(mA-m) O_A + 2^(mB-m) O_B)
-      // / (2^(mA-m) lA + 2^(mB-m) lB), lse = m + log2(...).
-      const int q4 = (warp - 4) & 3;
-      if (t == 1) {
-        float* xs = reinterpret_cast<float*>(smem + L.stg + (warp - 4) * 4096);
-        xs[lane] = m_ref;
-        xs[32 + lane] = l;
-        ptx::tc_fence_before();
-        ptx::bar_sync(1 + q4, 64);   // (m, l) and O_B are ready
-        ptx::bar_sync(5 + q4, 64);   // tile A has read O_B (the next unit's PV may overwrite it)
-        sbase += nb;
-        continue;
-      }
-      float sA, sB = 0.f, lse2;       // O = sA O_A + sB O_B
-      {
-        ptx::bar_sync(1 + q4, 64);
-        ptx::tc_fence_after();
-        const float* xs = reinterpret_cast<const float*>(smem + L.stg + warp * 4096);   // tile B warp q4's tile
-        const float mB = xs[lane], lB = xs[32 + lane];
-        const float mx = fmaxf(m_ref, mB);
-        const float mu = mx == -INFINITY ? 0.f : mx;
-        const float aA = m_ref == -INFINITY ? 0.f : ptx::ex2(m_ref - mu);
-        const float aB = mB == -INFINITY ? 0.f : ptx::ex2(mB - mu);
-        const float lt = l * aA + lB * aB;
-        const float iv = lt > 0.f ? 1.f / lt : 0.f;
-        sA = aA * iv;
-        sB = aB * iv;
-        lse2 = lt > 0.f ? mu + log2f(lt) : -INFINITY;
-      }
-      const float inv = 1.f;
-      // O / l leaves through a per-warp smem staging tile (XOR-swizzled 16-B units, no
-      // bank conflicts), so that every global store instruction writes whole row
-      // segments of 4 rows instead of 32 scattered pieces.  Row kinds: 2 = fp32 partial
-      // row, 1 = bf16 output row (DIRECT), 0 = nothing.  A warp whose rows are all bf16
-      // outputs (or nothing) stages 64 columns as bf16 per pass (one 128-B line per row:
-      // every STG.128 writes 4 whole lines); a warp with partial rows stages 32 fp32
-      // columns per pass.
-      {
-        const int kind = tgt == PM_DIRECT ? 1 : (tgt >= 0 ? 2 : 0);
-        char* rowp = kind == 1 ? reinterpret_cast<char*>(p.out) + ((int64_t)token * p.hq + head) * D * 2
-                   : kind == 2 ? reinterpret_cast<char*>(p.ws_o + ((int64_t)tgt * p.hq + head) * D) : nullptr;
-        const uint32_t stg = ptx::smem_u32(smem + L.stg + (warp - 4) * 4096);
-        const int k8 = lane & 7;
-        char* rp[8];
-        int rk[8];
-#pragma unroll
-        for (int s_ = 0; s_ < 8; ++s_) {          // rows s_ * 4 + lane / 8 of this warp, for the copy-out
-          const int rr = s_ * 4 + (lane >> 3);
-          rp[s_] = reinterpret_cast<char*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(rowp), rr));
-          rk[s_] = __shfl_sync(0xffffffffu, kind, rr);
-        }
-        const bool all_bf16 = __all_sync(0xffffffffu, kind != 2);
-        // TMEM column loads two chunks at a time (one wait per 64 columns), then through
-        // the staging tile
-#pragma unroll 1
-        for (int hh = 0; hh < D / 64; ++hh) {
-         uint32_t ov2[64];
-         ptx::tmem_ld32(tmem + lane_base + col_o + hh * 64, ov2);
-         ptx::tmem_ld32(tmem + lane_base + col_o + hh * 64 + 32, ov2 + 32);
-         {           // sA O_A + sB O_B (inv = 1 below)
-           uint32_t ob2[64];
-           ptx::tmem_ld32(tmem + lane_base + 256 + D + hh * 64, ob2);
-           ptx::tmem_ld32(tmem + lane_base + 256 + D + hh * 64 + 32, ob2 + 32);
-           ptx::tmem_wait_ld();
-#pragma unroll
-           for (int k = 0; k < 64; ++k)
-             ov2[k] = __float_as_uint(fmaf(__uint_as_float(ob2[k]), sB, __uint_as_float(ov2[k]) * sA));
-         }
-         ptx::tmem_wait_ld();
-         if (hh == 0 && threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 62);
-         if (all_bf16) {
-#pragma unroll
-          for (int u8 = 0; u8 < 8; ++u8) {
-            const uint32_t* o8 = ov2 + 8 * u8;
-            ptx::sts128u(stg + ptx::sw128(lane, u8),
-                         ptx::pack_bf16(__uint_as_float(o8[0]) * inv, __uint_as_float(o8[1]) * inv),
-                         ptx::pack_bf16(__uint_as_float(o8[2]) * inv, __uint_as_float(o8[3]) * inv),
-                         ptx::pack_bf16(__uint_as_float(o8[4]) * inv, __uint_as_float(o8[5]) * inv),
-                         ptx::pack_bf16(__uint_as_float(o8[6]) * inv, __uint_as_float(o8[7]) * inv));
-          }
-          __syncwarp();
-          uint4 v[8];   // all eight row segments in flight before the first store
-#pragma unroll
-          for (int s_ = 0; s_ < 8; ++s_) v[s_] = ptx::lds128u(stg + ptx::sw128(s_ * 4 + (lane >> 3), k8));
-#pragma unroll
-          for (int s_ = 0; s_ < 8; ++s_)
-            if (rk[s_] == 1) ptx::stg128u(rp[s_] + hh * 128 + k8 * 16, v[s_]);
-          __syncwarp();   // the staging tile is rewritten by the next chunk
-          continue;
-         }
-#pragma unroll
-         for (int cc = 0; cc < 2; ++cc) {
-          const int c = 2 * hh + cc;
-          const uint32_t* ov = ov2 + 32 * cc;
-#pragma unroll
-          for (int u8 = 0; u8 < 8; ++u8)
-            ptx::sts128(stg + ptx::sw128(lane, u8), __uint_as_float(ov[4 * u8]) * inv,
-                        __uint_as_float(ov[4 * u8 + 1]) * inv, __uint_as_float(ov[4 * u8 + 2]) * inv,
-                        __uint_as_float(ov[4 * u8 + 3]) * inv);
-          __syncwarp();
-          float4 v[8];   // all eight row segments in flight before the first store
-#pragma unroll
-          for (int s_ = 0; s_ < 8; ++s_) v[s_] = ptx::lds128(stg + ptx::sw128(s_ * 4 + (lane >> 3), k8));
-#pragma unroll
-          for (int s_ = 0; s_ < 8; ++s_) {
-            if (rk[s_] == 2)
-              ptx::stg128(rp[s_] + c * 128 + k8 * 16, v[s_]);
-            else if (rk[s_] == 1)
-              ptx::stg64(rp[s_] + c * 64 + k8 * 8, ptx::pack_bf16(v[s_].x, v[s_].y), ptx::pack_bf16(v[s_].z, v[s_].w));
-          }
-          __syncwarp();   // the staging tile is rewritten by the next chunk
-          if (c == 0 && threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 63);
-         }
-        }
-      }
-      {                               // O_B has been read: tile B may go on (its next PV overwrites O_B)
-        ptx::tc_fence_before();
-        ptx::bar_sync(5 + q4, 64);
-      }
-      if (threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 61);
-      if (tgt == PM_DIRECT) p.lse[(int64_t)token * p.hq + head] = lse2 * kLn2;
-      else if (tgt >= 0) p.ws_lse[(int64_t)tgt * p.hq + head] = lse2;
-      ptx::tc_fence_before();
-      if (threadIdx.x == 128 && ui == (int)blockIdx.x) trace_stamp(p, 5);
 #if BLEND_TRACE_UNITS
       if (threadIdx.x == 128 && uk < 10) trace_stamp(p, 23 + 4 * uk);
       cu_prev_end = clock64();
       cu_acc[2] += cu_prev_end - cu_lp;
 #endif
-      sbase += nb;
+    }
+    if (ep_pending) {
+      uint32_t ov[D];
+      ep_read(ov);
+      ep_store(ov);
     }
 #if BLEND_TRACE_UNITS
     if (threadIdx.x == 128 && p.trace != nullptr) {
@@ -771,13 +758,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1)
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, DN_TMEM_COLS);
   }
-  // this grid (a PDL dependent of the streaming grid, itself a dependent of the two-tile
-  // dense grid) completes only after both, so the merge grid that depends on it sees every
-  // partial row
-  ptx::pdl_wait();
 }
-
-}  // namespace ks
 
 cudaError_t make_cache_tmap(CUtensorMap* m, const void* base, int64_t rows, int D, int box_rows);
 cudaError_t make_q_tmap(CUtensorMap* m, const void* base, int64_t T, int hq, int D, int g, int box_tok);
@@ -785,7 +766,7 @@ cudaError_t set_smem_once(const void* func, size_t bytes);
 int num_sms_cached();
 
 template <int D, int BOX>
-static cudaError_t launch_dense_ks_db(const AttnParams& p, int64_t n_cache_pages, cudaStream_t st, bool overlap) {
+static cudaError_t launch_dense_db(const AttnParams& p, int64_t n_cache_pages, cudaStream_t st) {
   CUtensorMap tk, tv;
   const int64_t rows = n_cache_pages * p.hkv * p.ps;
   cudaError_t e = make_cache_tmap(&tk, p.k_cache, rows, D, BOX);
@@ -800,35 +781,28 @@ static cudaError_t launch_dense_ks_db(const AttnParams& p, int64_t n_cache_pages
     if (e == cudaSuccess) e = make_q_tmap(&tq1, p.q, p.n_tokens, p.hq, D, p.g, 1);
     if (e != cudaSuccess) return e;
   }
-  const size_t smem = ks::dense_layout(D).total + 1024;
-  e = set_smem_once((const void*)ks::dense_ks_kernel<D, BOX>, smem);
+  const size_t smem = dense_layout(D).total + 1024;
+  e = set_smem_once((const void*)dense_kernel<D, BOX>, smem);
   if (e != cudaSuccess) return e;
-  const int grid = p.n_units < num_sms_cached() ? p.n_units : num_sms_cached();
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(ks::DN_THREADS);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = overlap ? 1 : 0;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, ks::dense_ks_kernel<D, BOX>, tk, tv, tq, tq1, p);
+  int grid = p.n_units < num_sms_cached() ? p.n_units : num_sms_cached();
+  if (p.dense_ctas > 0 && grid > p.dense_ctas) grid = p.dense_ctas;   // planner: SMs left to streaming
+  dense_kernel<D, BOX><<<grid, DN_THREADS, smem, st>>>(tk, tv, tq, tq1, p);
+  return cudaPeekAtLastError();
 }
 
 template <int D>
-static cudaError_t launch_dense_ks_d(const AttnParams& p, int64_t n_cache_pages, cudaStream_t st, bool overlap) {
-  if (p.ps >= 64) return launch_dense_ks_db<D, 64>(p, n_cache_pages, st, overlap);
-  if (p.ps == 32) return launch_dense_ks_db<D, 32>(p, n_cache_pages, st, overlap);
-  return launch_dense_ks_db<D, 16>(p, n_cache_pages, st, overlap);
+static cudaError_t launch_dense_d(const AttnParams& p, int64_t n_cache_pages, cudaStream_t st) {
+  if (p.ps >= 64) return launch_dense_db<D, 64>(p, n_cache_pages, st);
+  if (p.ps == 32) return launch_dense_db<D, 32>(p, n_cache_pages, st);
+  return launch_dense_db<D, 16>(p, n_cache_pages, st);
 }
 
-// Key-split units (planner section SEC_DENSE_KS); p.units / p.dqtok / p.n_units describe them.
-cudaError_t launch_dense_ks(const AttnParams& p, int64_t n_cache_pages, cudaStream_t st, bool overlap) {
+cudaError_t launch_generic(const AttnParams& p, cudaStream_t st);
+
+cudaError_t launch_dense(const AttnParams& p, int64_t n_cache_pages, cudaStream_t st) {
   if (p.n_units <= 0) return cudaSuccess;
-  return p.d == 128 ? launch_dense_ks_d<128>(p, n_cache_pages, st, overlap)
-                    : launch_dense_ks_d<64>(p, n_cache_pages, st, overlap);
+  if (p.kv_f32) return launch_generic(p, st);
+  return p.d == 128 ? launch_dense_d<128>(p, n_cache_pages, st) : launch_dense_d<64>(p, n_cache_pages, st);
 }
 
 }  // namespace blend
