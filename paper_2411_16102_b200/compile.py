@@ -49,7 +49,7 @@ def _compile(src, verbose):
     cmd = [NVCC] + COMMON + [f"-D{d}" for d in DEFINES] + ARCH + ["-Xptxas", "-v" if verbose else "-O3", "-c", path, "-o", obj]
     if src.endswith(".cpp"):
         cmd = ["g++", "-std=c++17", "-O3", "-g", "-fPIC", "-Wall", "-I", os.path.join(ROOT, "include"),
-               "-I", CSRC, "-c", path, "-o", obj]
+               "-I", CSRC] + [f"-D{d}" for d in DEFINES] + ["-c", path, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"compile failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")

@@ -25,6 +25,10 @@
 #include "internal.h"
 #include "tree.h"
 
+#ifndef BLEND_STREAM_SM_GBS
+#define BLEND_STREAM_SM_GBS 68.0   // planning constant: streaming pass GB/s per SM on a partial grid
+#endif
+
 namespace {
 
 thread_local std::string g_err;
@@ -586,15 +590,20 @@ int build_plan(blend_tree* t) {
   // dense, ~6 TB/s streaming; a 250 TFLOP/s estimate gave the dense pass twice the SMs
   // the streaming pass could spare: C2 47.3 us with 64 dense CTAs, 43.7 us with 32).
   // When the dense pass alone would fill the GPU and both passes are substantial, cap
-  // its grid so the overlapped streaming grid starts on the remaining SMs at once
-  // (measured on B200: C4 -2 %, C5 -3 % with caps near these shares; the share moves
-  // from 0.4 toward 1 as the dense estimate dominates).  Rates: ~690 TFLOP/s dense,
-  // ~6.9 TB/s streaming (round-1 measurements).
+  // its grid so the overlapped streaming grid starts on the remaining SMs at once.  The
+  // cap is the dense pass's share of the SM-time: a = (dense time on the whole GPU) x
+  // SMs, b = streaming bytes / (per-SM streaming rate), D = SMs x a / (a + b), so that
+  // both grids finish together.  On fewer SMs the streaming pass is bound by its
+  // consumer warps (~BLEND_STREAM_SM_GBS per SM, well under an SM's share of HBM), not
+  // by HBM.  Rates: ~690 TFLOP/s dense (round-1), 68 GB/s per SM streaming (one
+  // consumer warp per SM streams C4 at 17 GB/s, round 2).
   t->dense_ctas = 0;
   if (base_d >= num_sms && flops_d > 0.0 && bytes_s > 0.0) {
     const double td = flops_d / 690e12, ts = bytes_s / 6.9e12;
-    if (td > 0.2 * (td + ts) && ts > 0.2 * (td + ts))
-      t->dense_ctas = (int32_t)((0.4 + 0.6 * td / (td + ts)) * num_sms + 0.5);
+    if (td > 0.2 * (td + ts) && ts > 0.2 * (td + ts)) {
+      const double a = td * num_sms, b = bytes_s / (BLEND_STREAM_SM_GBS * 1e9);
+      t->dense_ctas = (int32_t)(num_sms * a / (a + b) + 0.5);
+    }
   }
   int64_t dsplit = 1;
   if (a.dense_split > 0) dsplit = a.dense_split;

@@ -1,3 +1,7 @@
+// streamw_transposed.cu — EXPERIMENT (not built): the streaming consumer in transposed form
+// (keys as the MMA's M, rows as N).  Measured slower per consumer warp (C4, one warp per SM:
+// 40.1 vs 25.0 ms); see profiles/r2_dense_experiments/README.md.
+//
 // streamw.cu — streaming pass, warp-per-unit form (the default streaming kernel).
 //
 // Same contract as stream.cu (SMALL units: <= 16 rows of one kv head over their page
@@ -24,6 +28,17 @@
 #include "ptx.cuh"
 
 namespace blend {
+namespace ptx {
+// 8x8 b16 transpose across the warp: lane (r, c) of the fragment gets element (c, r)
+__device__ __forceinline__ uint32_t movm_t(uint32_t a) {
+  uint32_t d;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(d) : "r"(a));
+  return d;
+}
+}  // namespace ptx
+}  // namespace blend
+
+namespace blend {
 
 #ifndef BLEND_TRACE_STAGES
 #define BLEND_TRACE_STAGES 0   // 1: per-stage stamps (stages 4..11 of ring 0) in the diagnostics trace
@@ -32,6 +47,9 @@ namespace blend {
 #ifndef SW_WARPS_CFG
 #define SW_WARPS_CFG 4
 #define SW_STAGES_CFG 3
+#endif
+#ifndef SW_TRANSPOSED
+#define SW_TRANSPOSED 1   // keys as the MMA's M, rows as N (decode units: half the MMAs)
 #endif
 #ifndef SW_Q_AFTER
 #define SW_Q_AFTER 1   // the next unit's Q rows are requested after this many stages of the current one
@@ -265,6 +283,19 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
     const Pre cu = pre;
     ptx::cp_async_wait_group0();
     __syncwarp();
+#if SW_TRANSPOSED
+    // Q^T as the B operand of S^T = K Q^T: qb[n][kk] = row 8n + g8, dims 16kk + 2c4 (+1) and + 8
+    uint32_t qb[2][D / 16][2];
+#pragma unroll
+    for (int n = 0; n < 2; ++n)
+#pragma unroll
+      for (int kk = 0; kk < D / 16; kk += 2) {
+        const int row = 8 * n + (lane & 7);
+        const int unit16 = 2 * kk + (lane >> 3);
+        ptx::ldsm_x4(qs_u32 + buf * (CH * 2048) + (unit16 / 8) * 2048 + ptx::sw128(row, unit16 % 8), qb[n][kk][0],
+                     qb[n][kk][1], qb[n][kk + 1][0], qb[n][kk + 1][1]);
+      }
+#else
     uint32_t qa[D / 16][4];
 #pragma unroll
     for (int kk = 0; kk < D / 16; ++kk) {
@@ -274,6 +305,7 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
       ptx::ldsm_x4(qs_u32 + buf * (CH * 2048) + (unit16 / 8) * 2048 + ptx::sw128(row, unit16 % 8), qa[kk][0],
                    qa[kk][1], qa[kk][2], qa[kk][3]);
     }
+#endif
     __syncwarp();   // every lane's ldmatrix of this buffer is done before the next prefetch targets it later
     nann = next_index();
     bool q_pending = nann.x < p.n_units;
@@ -282,10 +314,31 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
     const int32_t pos0r = cu.d0.qrow >= 0 ? cu.d0.pos : INT32_MIN;
     const int32_t pos1r = cu.d1.qrow >= 0 ? cu.d1.pos : INT32_MIN;
 
+#if SW_TRANSPOSED
+    // Transposed form (keys as the MMA's M, the unit's rows as N = 8 per n-tile): a decode
+    // unit of g <= 8 rows needs one n-tile, half the MMAs of the rows-as-M form.
+    const int nn = __any_sync(0xffffffffu, cu.d1.qrow >= 0) ? 2 : 1;   // 8-row n-tiles in use
+    int32_t rpos[2][2];   // positions of this lane's score columns: rows 8n + 2c4 + r
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int src = 4 * (2 * c4 + r);   // lanes 4g..4g+3 hold row g (d0) and row g + 8 (d1)
+      rpos[0][r] = __shfl_sync(0xffffffffu, pos0r, src);
+      rpos[1][r] = __shfl_sync(0xffffffffu, pos1r, src);
+    }
+    float ot[D / 16][2][4];   // O^T: dims 16dt + g8 (c0, c1) and + 8 (c2, c3), rows 8n + 2c4 (+1)
+#pragma unroll
+    for (int dt = 0; dt < D / 16; ++dt)
+#pragma unroll
+      for (int n = 0; n < 2; ++n) ot[dt][n][0] = ot[dt][n][1] = ot[dt][n][2] = ot[dt][n][3] = 0.f;
+    float mr[2][2], lr[2][2];   // running max (log2 domain) and this lane's partial sum, per row
+#pragma unroll
+    for (int n = 0; n < 2; ++n) mr[n][0] = mr[n][1] = -INFINITY, lr[n][0] = lr[n][1] = 0.f;
+#else
     float o[NT][4];
 #pragma unroll
     for (int j = 0; j < NT; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
     float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+#endif
 
     int4 eb_cur = cu.ebatch, eb_nxt = make_int4(0, 0, 0, 0);
     if (cu.ne > 32) eb_nxt = lane + 32 < cu.ne ? ents[cu.eb + 32 + lane] : make_int4(0, 0, 0, 0);
@@ -322,6 +375,125 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
 #endif
         const uint32_t kst = ptx::smem_u32(ring + s * L.stage_stride);
         const uint32_t vst = kst + CH * SW_CHUNK;
+#if SW_TRANSPOSED
+        const int mtv = nvalid > 16 ? 2 : 1;   // 16-key m-tiles holding valid keys
+        // S^T = K Q^T; two accumulators per (m-tile, n-tile) split the 8-step k chain
+        float st[2][2][4], st2[2][2][4];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int n = 0; n < 2; ++n)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) st[mt][n][c] = st2[mt][n][c] = 0.f;
+        auto qk_t = [&](int mt, int kk) {
+          const int row = 16 * mt + (lane & 7) + ((lane >> 3) & 1) * 8;   // key
+          const int unit16 = 2 * kk + (lane >> 4);
+          uint32_t a[4];
+          ptx::ldsm_x4(kst + (unit16 / 8) * SW_CHUNK + ptx::sw128(row, unit16 % 8), a[0], a[1], a[2], a[3]);
+          float(&acc)[2][4] = (kk & 1) ? st2[mt] : st[mt];
+          ptx::mma_bf16_16816(acc[0], a, qb[0][kk][0], qb[0][kk][1]);
+          if (nn == 2) ptx::mma_bf16_16816(acc[1], a, qb[1][kk][0], qb[1][kk][1]);
+        };
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          qk_t(0, kk);
+          if (mtv == 2) qk_t(1, kk);
+        }
+        // mask, scale, per-row max over the stage's keys (the key lanes g8 = 0..7)
+        float mx[2][2];
+#pragma unroll
+        for (int n = 0; n < 2; ++n) {
+          mx[n][0] = mx[n][1] = -INFINITY;
+          if (n >= nn) break;
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const int key = 16 * mt + g8 + (c >> 1) * 8;
+              const int kp = en_pos0 + kbase + key;
+              const float v = st[mt][n][c] + st2[mt][n][c];
+              st[mt][n][c] = (key < nvalid && kp <= rpos[n][c & 1]) ? v * p.scale_log2 : -INFINITY;
+              mx[n][c & 1] = fmaxf(mx[n][c & 1], st[mt][n][c]);
+            }
+        }
+#pragma unroll
+        for (int n = 0; n < 2; ++n)
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            if (n >= nn) break;
+            mx[n][r] = fmaxf(mx[n][r], __shfl_xor_sync(0xffffffffu, mx[n][r], 4));
+            mx[n][r] = fmaxf(mx[n][r], __shfl_xor_sync(0xffffffffu, mx[n][r], 8));
+            mx[n][r] = fmaxf(mx[n][r], __shfl_xor_sync(0xffffffffu, mx[n][r], 16));
+          }
+        if (p.stats != nullptr) {   // diagnostics: stages, and stages that rescale a live row's O
+          bool rs = false;
+#pragma unroll
+          for (int n = 0; n < 2; ++n)
+#pragma unroll
+            for (int r = 0; r < 2; ++r) rs = rs || (n < nn && mr[n][r] != -INFINITY && mx[n][r] > mr[n][r]);
+          const bool any_rs = __any_sync(0xffffffffu, rs);
+          if (lane == 0) {
+            stat_add(p, STAT_STREAM_STAGES, 1);
+            if (any_rs) stat_add(p, STAT_STREAM_RESCALE, 1);
+            if (tail) stat_add(p, STAT_TAIL_ZEROED, 1);
+          }
+        }
+        float al[2][2];
+#pragma unroll
+        for (int n = 0; n < 2; ++n)
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            const float mn = fmaxf(mr[n][r], mx[n][r]);
+            const float mu = mn == -INFINITY ? 0.f : mn;
+            al[n][r] = ptx::ex2(mr[n][r] - mu);
+            mr[n][r] = mn;
+            mx[n][r] = mu;   // the exponent reference of this stage
+          }
+        // P^T = 2^(S^T - m): B operands of O^T += V^T P^T by transposing 8x8 bf16 blocks
+        uint32_t pb[2][2][2];
+#pragma unroll
+        for (int n = 0; n < 2; ++n) {
+          if (n >= nn) break;
+          float ps0 = 0.f, ps1 = 0.f;
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) st[mt][n][c] = ptx::ex2(st[mt][n][c] - mx[n][c & 1]);
+            ps0 += st[mt][n][0] + st[mt][n][2];
+            ps1 += st[mt][n][1] + st[mt][n][3];
+            pb[mt][n][0] = ptx::movm_t(ptx::pack_bf16(st[mt][n][0], st[mt][n][1]));   // keys 16mt + 0..7
+            pb[mt][n][1] = ptx::movm_t(ptx::pack_bf16(st[mt][n][2], st[mt][n][3]));   // keys 16mt + 8..15
+          }
+          lr[n][0] = lr[n][0] * al[n][0] + ps0;
+          lr[n][1] = lr[n][1] * al[n][1] + ps1;
+        }
+#pragma unroll
+        for (int n = 0; n < 2; ++n) {
+          if (n >= nn) break;
+#pragma unroll
+          for (int dt = 0; dt < D / 16; ++dt) {
+            ot[dt][n][0] *= al[n][0];
+            ot[dt][n][1] *= al[n][1];
+            ot[dt][n][2] *= al[n][0];
+            ot[dt][n][3] *= al[n][1];
+          }
+        }
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          if (mt >= mtv) break;
+#pragma unroll
+          for (int dt = 0; dt < D / 16; ++dt) {
+            const int mi = lane >> 3;
+            const int row = mt * 16 + (mi & 1) * 8 + (lane & 7);   // key
+            const int unit16 = 2 * dt + (mi >> 1);
+            uint32_t v0, v1, v2, v3;
+            ptx::ldsm_x4_t(vst + (unit16 / 8) * SW_CHUNK + ptx::sw128(row, unit16 % 8), v0, v1, v2, v3);
+            const uint32_t a[4] = {v0, v2, v1, v3};   // V^T: dims 16dt + (0..7 | 8..15) x keys 16mt + ...
+            ptx::mma_bf16_16816(ot[dt][0], a, pb[mt][0][0], pb[mt][0][1]);
+            if (nn == 2) ptx::mma_bf16_16816(ot[dt][1], a, pb[mt][1][0], pb[mt][1][1]);
+          }
+        }
+#else
         const int ntv = nvalid >= SW_KEYS ? 4 : (nvalid + 7) / 8;   // n-tiles holding valid keys
         const int nkv = nvalid > 16 ? 2 : 1;                         // 16-key k-steps for PV
         float sc[4][4];
@@ -420,6 +592,7 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
             ptx::mma_bf16_16816(o[j + 1], pa, b2, b3);
           }
         }
+#endif
         if (tail) ptx::fence_proxy_async_smem();   // generic zero stores before the next TMA write
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&wempty[s]);
@@ -434,6 +607,62 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
     }
     if (q_pending) issue_q(pre, buf ^ 1);
     if (warp == 0 && lane == 0) trace_stamp_s(p, 4 + 4 * tu);
+#if SW_TRANSPOSED
+    // ---- unit end: full row sums over the key lanes, then O^T back to rows by 8x8
+    // transposes: lane (g8, c4) gets row 8n + g8, dims 16dt + 2c4 (+1) and 16dt + 8 + 2c4 (+1)
+#pragma unroll
+    for (int n = 0; n < 2; ++n)
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        lr[n][r] += __shfl_xor_sync(0xffffffffu, lr[n][r], 4);
+        lr[n][r] += __shfl_xor_sync(0xffffffffu, lr[n][r], 8);
+        lr[n][r] += __shfl_xor_sync(0xffffffffu, lr[n][r], 16);
+      }
+#pragma unroll
+    for (int n = 0; n < 2; ++n) {
+      if (n >= nn) break;
+      float inv[2], lse[2];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        inv[r] = lr[n][r] > 0.f ? 1.f / lr[n][r] : 0.f;
+        lse[r] = lr[n][r] > 0.f ? (mr[n][r] == -INFINITY ? 0.f : mr[n][r]) + log2f(lr[n][r]) : -INFINITY;
+      }
+      // this lane's output row 8n + g8: its lse comes from a lane holding that row's column
+      const float la = __shfl_sync(0xffffffffu, lse[0], g8 >> 1), lb = __shfl_sync(0xffffffffu, lse[1], g8 >> 1);
+      const float lse2 = (g8 & 1) ? lb : la;
+      const RowDesc d = n ? cu.d1 : cu.d0;
+      const bool live = d.qrow >= 0 && d.target != PM_SKIP;
+      const bool direct = d.target == PM_DIRECT;
+      if (__any_sync(0xffffffffu, live && !direct)) {
+        // fp32 rows: the 32-bit values cross the transpose as two 16-bit planes
+        float* dst = p.ws_o + ((int64_t)d.target * p.hq + d.head) * D;
+#pragma unroll
+        for (int dt = 0; dt < D / 16; ++dt)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t u0 = __float_as_uint(ot[dt][n][2 * h] * inv[0]);
+            const uint32_t u1 = __float_as_uint(ot[dt][n][2 * h + 1] * inv[1]);
+            const uint32_t lo = ptx::movm_t(__byte_perm(u0, u1, 0x5410));
+            const uint32_t hi = ptx::movm_t(__byte_perm(u0, u1, 0x7632));
+            if (live && !direct)
+              *reinterpret_cast<float2*>(dst + 16 * dt + 8 * h + 2 * c4) =
+                  make_float2(__uint_as_float(__byte_perm(lo, hi, 0x5410)), __uint_as_float(__byte_perm(lo, hi, 0x7632)));
+          }
+        if (live && !direct && c4 == 0) p.ws_lse[(int64_t)d.target * p.hq + d.head] = lse2;
+      }
+      if (__any_sync(0xffffffffu, live && direct)) {
+        __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.out) + (int64_t)(d.qrow >= 0 ? d.qrow : 0) * D;
+#pragma unroll
+        for (int dt = 0; dt < D / 16; ++dt)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t v = ptx::movm_t(ptx::pack_bf16(ot[dt][n][2 * h] * inv[0], ot[dt][n][2 * h + 1] * inv[1]));
+            if (live && direct) *reinterpret_cast<uint32_t*>(dst + 16 * dt + 8 * h + 2 * c4) = v;
+          }
+        if (live && direct && c4 == 0) p.lse[d.qrow] = lse2 * kLn2;
+      }
+    }
+#else
     // ---- unit end: rows g8 (o[.][0,1]) and g8+8 (o[.][2,3]) straight from the fragments
     l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
     l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
@@ -462,6 +691,7 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
         if (c4 == 0) p.ws_lse[(int64_t)d.target * p.hq + d.head] = lse2;
       }
     }
+#endif
     if (warp == 0 && lane == 0) trace_stamp_s(p, 5 + 4 * tu);
   }
   ptx::pdl_wait();
