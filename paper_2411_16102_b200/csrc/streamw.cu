@@ -339,10 +339,23 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
           ptx::mma_bf16_16816(sc[nt], qa[kk + 1], b2, b3);
         };
         if (ntv == 4) {
+          // the four n-tiles' K fragments of a k-step pair are requested before any MMA uses
+          // them (ldmatrix and mma.sync issue in source order)
 #pragma unroll
-          for (int kk = 0; kk < D / 16; kk += 2)
+          for (int kk = 0; kk < D / 16; kk += 2) {
+            uint32_t kb[4][4];
 #pragma unroll
-            for (int nt = 0; nt < 4; ++nt) qk_step(nt, kk);
+            for (int nt = 0; nt < 4; ++nt) {
+              const int row = nt * 8 + (lane & 7);
+              const int unit16 = 2 * kk + (lane >> 3);
+              ptx::ldsm_x4(kst + (unit16 / 8) * SW_CHUNK + ptx::sw128(row, unit16 % 8), kb[nt][0], kb[nt][1], kb[nt][2],
+                           kb[nt][3]);
+            }
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) ptx::mma_bf16_16816(sc[nt], qa[kk], kb[nt][0], kb[nt][1]);
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) ptx::mma_bf16_16816(sc[nt], qa[kk + 1], kb[nt][2], kb[nt][3]);
+          }
         } else {
 #pragma unroll
           for (int nt = 0; nt < 4; ++nt) {
@@ -409,15 +422,23 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
           pa[1] = ptx::pack_bf16(sc[2 * ks][2], sc[2 * ks][3]);
           pa[2] = ptx::pack_bf16(sc[2 * ks + 1][0], sc[2 * ks + 1][1]);
           pa[3] = ptx::pack_bf16(sc[2 * ks + 1][2], sc[2 * ks + 1][3]);
+          // V fragments of four 16-column pairs in flight before their MMAs
 #pragma unroll
-          for (int j = 0; j < NT; j += 2) {
-            const int mi = lane >> 3;
-            const int row = ks * 16 + (mi & 1) * 8 + (lane & 7);
-            const int unit16 = j + (mi >> 1);
-            uint32_t b0, b1, b2, b3;
-            ptx::ldsm_x4_t(vst + (unit16 / 8) * SW_CHUNK + ptx::sw128(row, unit16 % 8), b0, b1, b2, b3);
-            ptx::mma_bf16_16816(o[j], pa, b0, b1);
-            ptx::mma_bf16_16816(o[j + 1], pa, b2, b3);
+          for (int j0 = 0; j0 < NT; j0 += 8) {
+            uint32_t vb[4][4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int mi = lane >> 3;
+              const int row = ks * 16 + (mi & 1) * 8 + (lane & 7);
+              const int unit16 = j0 + 2 * q + (mi >> 1);
+              ptx::ldsm_x4_t(vst + (unit16 / 8) * SW_CHUNK + ptx::sw128(row, unit16 % 8), vb[q][0], vb[q][1], vb[q][2],
+                             vb[q][3]);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              ptx::mma_bf16_16816(o[j0 + 2 * q], pa, vb[q][0], vb[q][1]);
+              ptx::mma_bf16_16816(o[j0 + 2 * q + 1], pa, vb[q][2], vb[q][3]);
+            }
           }
         }
         if (tail) ptx::fence_proxy_async_smem();   // generic zero stores before the next TMA write
