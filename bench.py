@@ -253,7 +253,10 @@ def _roofline(kind, pw, t_ms, peaks, burst, workload, path_auto):
                 "bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak,
                 "traffic": traffic, "traffic_source": tsrc, "launch_ms": t_ms,
                 "algorithmic_per_launch": pw["dense_flops"], "algorithmic_bytes_per_launch": pw["dense_bytes"],
-                "peak_source": peaks["_source"] + (" bf16 burst" if burst else " bf16 sustained")}
+                "peak_source": peaks["_source"] + (" bf16 burst" if burst else " bf16 sustained"),
+                # context: the same achieved rate against the power-capped sustained GEMM figure
+                # (the timed region is ~1 s of back-to-back steps; `frac` keeps the burst peak)
+                "frac_vs_sustained": tf / peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])}
     gbs = pw["stream_bytes"] / (t_ms * 1e-3) / 1e9 if t_ms > 0 else 0.0
     peak = peaks["hbm_gbs"]
     traffic, tsrc = ncu_traffic(workload, "streamw_kernel") if path_auto else (None, None)
