@@ -33,6 +33,9 @@ namespace blend {
 #define SW_WARPS_CFG 4
 #define SW_STAGES_CFG 3
 #endif
+#ifndef SW_EVICT_FIRST
+#define SW_EVICT_FIRST 1   // streaming K/V loads carry an L2 evict-first policy
+#endif
 #ifndef SW_Q_AFTER
 #define SW_Q_AFTER 1   // the next unit's Q rows are requested after this many stages of the current one
 #endif
@@ -102,6 +105,9 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
       ptx::tma_prefetch_desc(&tmk16);
       ptx::tma_prefetch_desc(&tmv16);
       const int4* ents = reinterpret_cast<const int4*>(p.entries);
+#if SW_EVICT_FIRST
+      const uint64_t pol = ptx::l2_policy_evict_first();
+#endif
       uint64_t* rfull = full + w * SW_STAGES;
       uint64_t* rempty = empty + w * SW_STAGES;
       uint8_t* ring = smem + L.ring0 + w * L.ring_stride;
@@ -171,6 +177,18 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
             ptx::mbar_arrive_expect_tx(&rfull[s], 2u * CH * rows * 128u);
 #pragma unroll
             for (int c = 0; c < CH; ++c) {
+#if SW_EVICT_FIRST
+              // a streaming unit's K/V (a request's private suffix) is read once: evict-first,
+              // so it does not push the dense pass's re-read K/V (shared prefixes, the 8 row
+              // units of a prefill chunk) out of L2 while the two passes overlap
+              if (rows == SW_KEYS) {
+                ptx::tma_load_2d_hint(st + c * SW_CHUNK, &tmk32, &rfull[s], c * 64, y, pol);
+                ptx::tma_load_2d_hint(st + (CH + c) * SW_CHUNK, &tmv32, &rfull[s], c * 64, y, pol);
+              } else {
+                ptx::tma_load_2d_hint(st + c * SW_CHUNK, &tmk16, &rfull[s], c * 64, y, pol);
+                ptx::tma_load_2d_hint(st + (CH + c) * SW_CHUNK, &tmv16, &rfull[s], c * 64, y, pol);
+              }
+#else
               if (rows == SW_KEYS) {
                 ptx::tma_load_2d(st + c * SW_CHUNK, &tmk32, &rfull[s], c * 64, y);
                 ptx::tma_load_2d(st + (CH + c) * SW_CHUNK, &tmv32, &rfull[s], c * 64, y);
@@ -178,6 +196,7 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
                 ptx::tma_load_2d(st + c * SW_CHUNK, &tmk16, &rfull[s], c * 64, y);
                 ptx::tma_load_2d(st + (CH + c) * SW_CHUNK, &tmv16, &rfull[s], c * 64, y);
               }
+#endif
             }
             advance();   // one pipeline step per issued stage, after its loads are in flight
           }
