@@ -59,7 +59,7 @@ def load_peaks():
     return d
 
 
-PROFILE_TAG = "r2k"   # profiles/<tag>_ncu.json: ncu --set full captures of this code's kernels
+PROFILE_TAG = "r2l"   # profiles/<tag>_ncu.json: ncu --set full captures of this code's kernels
 
 
 def ncu_traffic(workload: str, kernel: str):
