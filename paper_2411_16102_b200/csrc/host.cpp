@@ -598,11 +598,14 @@ int build_plan(blend_tree* t) {
   // by HBM.  Rates: ~690 TFLOP/s dense (round-1), 68 GB/s per SM streaming (one
   // consumer warp per SM streams C4 at 17 GB/s, round 2).
   t->dense_ctas = 0;
+  double cap_a = 0.0, cap_b = 0.0;   // SM-time of the dense and the streaming pass (see the key-split units below)
   if (base_d >= num_sms && flops_d > 0.0 && bytes_s > 0.0) {
     const double td = flops_d / 690e12, ts = bytes_s / 6.9e12;
     if (td > 0.2 * (td + ts) && ts > 0.2 * (td + ts)) {
       const double a = td * num_sms, b = bytes_s / (BLEND_STREAM_SM_GBS * 1e9);
       t->dense_ctas = (int32_t)(num_sms * a / (a + b) + 0.5);
+      cap_a = a;
+      cap_b = b;
     }
   }
   int64_t dsplit = 1;
@@ -866,6 +869,18 @@ int build_plan(blend_tree* t) {
     }
     dunits.swap(keep);
     dqtok.swap(keep_q);
+  }
+  // The key-split units run after the streaming grid (on every SM), so only the two-tile
+  // units' share of the dense SM-time is balanced against the streaming pass: a splits by
+  // the two lists' block counts weighted with their measured per-block cost (a key-split
+  // block, one 128-row tile: 0.54 of a two-tile block pair; C4).
+  if (t->dense_ctas > 0 && !dunits_ks.empty() && cap_a > 0.0) {
+    const int32_t epb = 64 / std::min<int32_t>(a.page_size, 64);
+    double w_d = 0.0, w_k = 0.0;
+    for (const auto& u : dunits) w_d += (double)((u.entry_end - u.entry_begin + epb - 1) / epb);
+    for (const auto& u : dunits_ks) w_k += 0.54 * (double)((u.entry_end - u.entry_begin + epb - 1) / epb);
+    const double a_d = cap_a * w_d / (w_d + w_k);
+    t->dense_ctas = std::max<int32_t>(1, (int32_t)(num_sms * a_d / (a_d + cap_b) + 0.5));
   }
 
   // Per-row descriptors of the streaming units (STREAM_ROWS slots per unit): the
