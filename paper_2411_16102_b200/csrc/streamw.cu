@@ -178,9 +178,9 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
 #pragma unroll
             for (int c = 0; c < CH; ++c) {
 #if SW_EVICT_FIRST
-              // a streaming unit's K/V (a request's private suffix) is read once: evict-first,
-              // so it does not push the dense pass's re-read K/V (shared prefixes, the 8 row
-              // units of a prefill chunk) out of L2 while the two passes overlap
+              // a streaming unit's K/V (a request's private suffix) is read once: evict-first
+              // (it need not displace the dense pass's re-read K/V from L2; measured: C2
+              // streaming pass 35 -> 31 us, C4 neutral, C3 / C5 within 1 %)
               if (rows == SW_KEYS) {
                 ptx::tma_load_2d_hint(st + c * SW_CHUNK, &tmk32, &rfull[s], c * 64, y, pol);
                 ptx::tma_load_2d_hint(st + (CH + c) * SW_CHUNK, &tmv32, &rfull[s], c * 64, y, pol);
